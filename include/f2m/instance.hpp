@@ -1,0 +1,3 @@
+// Compatibility include: the reference header f2m/instance.hpp maps onto the single B200 API header.
+#pragma once
+#include "f2m/api.hpp"

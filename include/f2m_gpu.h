@@ -1,0 +1,250 @@
+/*
+ * f2m_gpu.h — C ABI of the B200-native F2M gradient-descent-procedure (GDP) solver.
+ *
+ * This is the drop-in boundary of SURVEY.md §8(b): plain pointers and sizes, no C++ or
+ * torch types. Every compute entry point runs hand-written sm_100a CUDA kernels
+ * (libf2m_gpu.so); there is no CPU fallback — without a usable CUDA device every call
+ * returns F2M_E_CUDA.
+ *
+ * Each entry point names the reference interface it replaces (paths relative to
+ * /root/reference/proj). The host C++ mirror of the reference API (include/f2m/api.hpp,
+ * namespace f2m) and the pybind11 module _f2m are thin layers over these calls, so the
+ * reference's Python binding (python/bindings.cpp) and C++ headers keep working unchanged.
+ *
+ * Conventions
+ *  - All calls are blocking and return an int status (F2M_OK == 0). On failure
+ *    f2m_last_error() returns a thread-local message; the status maps 1:1 onto the
+ *    reference's exception taxonomy (include/f2m/errors.hpp:9-57).
+ *  - Arrays named h_* / unqualified are HOST memory, caller-owned. Arrays named d_* are
+ *    DEVICE memory (already resident in HBM) on the graph's device.
+ *  - Node ids and edge ids are the reference's: edges sorted by (u, v) with u < v
+ *    (graph.hpp:16-17), lambda indexed by node id. The device internally renumbers nodes
+ *    spatially (Morton order of the k-NN grid) — invisible at this boundary.
+ *  - A graph handle must not be used from two threads at once.
+ */
+#ifndef F2M_GPU_H
+#define F2M_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception type (errors.hpp) -------------------- */
+enum f2m_status {
+  F2M_OK = 0,
+  F2M_E_ARGUMENT = 1,       /* ArgumentError        errors.hpp:15  */
+  F2M_E_INDEX = 2,          /* IndexError           errors.hpp:20  */
+  F2M_E_MIN_DEGREE = 3,     /* MinDegreeError       errors.hpp:25  */
+  F2M_E_STRUCTURE = 4,      /* StructureError       errors.hpp:30  */
+  F2M_E_DEGREE = 5,         /* DegreeError          errors.hpp:35  */
+  F2M_E_DEGENERATE = 6,     /* DegenerateExtraction errors.hpp:41  */
+  F2M_E_SOLVE_FAILED = 7,   /* SolveFailed          errors.hpp:56  */
+  F2M_E_CUDA = 8,           /* CUDA runtime failure / no device (no CPU fallback exists) */
+  F2M_E_NOMEM = 9,          /* device allocation failure */
+  F2M_E_TIMEOUT = 10        /* device watchdog fired inside a persistent kernel */
+};
+
+/* Thread-local description of the last failure on this thread. */
+const char* f2m_last_error(void);
+
+/* Selects the CUDA device used by subsequent graph creations on this thread (default 0). */
+int f2m_set_device(int device);
+
+/* Library/device facts: SM count, persistent-sweep CTAs and threads, compile target. */
+typedef struct {
+  int device;
+  int sm_count;
+  int sweep_ctas;
+  int sweep_threads;
+  int cc_major;
+  int cc_minor;
+  char name[96];
+} f2m_device_info;
+int f2m_get_device_info(f2m_device_info* out);
+
+/* ---- graphs (graph.hpp:18-60) ----------------------------------------------------------
+ * An f2m_graph is a device-resident candidate graph: the sorted edge list (u, v, cost), a
+ * SELL-32 incidence layout in spatial node order for the GDP sweep, and its mean cost.  */
+typedef struct f2m_graph f2m_graph;
+
+/* Graph::from_edges (graph.cpp:14-51): endpoints normalized to u < v, stable-sorted by
+ * (u, v); duplicates and self-loops are kept for f2m_graph_validate. F2M_E_INDEX on an
+ * endpoint outside [0, n). */
+int f2m_graph_from_edges(int n, int64_t m, const int32_t* eu, const int32_t* ev,
+                         const double* cost, f2m_graph** out);
+
+/* build_knn_graph (graph.cpp:169-240): symmetrized k-NN graph of n points (xy[2i], xy[2i+1])
+ * under DistanceMode rounded (1 = EUC_2D nint, 0 = exact). Candidate lists are bit-exact
+ * with the reference. F2M_E_ARGUMENT for k < 3 or n < 4. */
+int f2m_knn_build(int n, const double* xy, int rounded, int k, f2m_graph** out);
+/* Same, with the points already resident in device memory (d_xy, 2n doubles). */
+int f2m_knn_build_device(int n, const double* d_xy, int rounded, int k, f2m_graph** out);
+
+/* Graph::with_costs (graph.cpp:53-65): same topology, new costs and mean cost. */
+int f2m_graph_with_costs(const f2m_graph* g, const double* cost, f2m_graph** out);
+
+/* jittered() (solve.cpp:39-47): costs + perturb_scale*cost_scale*U[0,1) from the
+ * SplitMix64 stream seeded seed*0x9E3779B97F4A7C15 + restart, one draw per edge in edge-id
+ * order — generated on the device, no host round trip of the topology. */
+int f2m_graph_jittered(const f2m_graph* g, uint64_t seed, int restart, double perturb_scale,
+                       f2m_graph** out);
+
+void f2m_graph_destroy(f2m_graph* g);
+
+typedef struct {
+  int n;
+  int64_t m;
+  double mean_cost;   /* Graph::mean_cost (graph.hpp:49): sequential sum / m, bit-exact */
+  int min_degree;
+  int max_degree;
+  int64_t sell_slots; /* padded SELL-32 slot count (>= 2m) */
+} f2m_graph_info;
+int f2m_graph_get_info(const f2m_graph* g, f2m_graph_info* out);
+
+/* Edge list download (Graph::edges, graph.hpp:30-31). Any pointer may be NULL. */
+int f2m_graph_edges(const f2m_graph* g, int32_t* eu, int32_t* ev, double* cost);
+/* Per-node degrees (Graph::degree, graph.hpp:38-41). */
+int f2m_graph_degrees(const f2m_graph* g, int32_t* degree);
+/* Reference CSR incidence (graph.cpp:27-45): offsets[n+1], ids[2m] edge ids ascending per
+ * row — for host-side Graph::incident(). */
+int f2m_graph_incidence(const f2m_graph* g, int64_t* offsets, int32_t* ids);
+
+/* validate_graph (graph.cpp:242-277): F2M_E_STRUCTURE on the first self-loop / duplicate /
+ * negative cost in edge order, F2M_E_MIN_DEGREE if the minimum degree is below 3. */
+int f2m_graph_validate(const f2m_graph* g, int* min_degree, int* max_degree, int64_t* edges);
+
+/* ---- dual engine (dual.hpp) ---------------------------------------------------------- */
+typedef struct {            /* EngineConfig, dual.hpp:29-40 */
+  int b;                    /* right-hand side, 1..8 (kMaxB, dual.cpp:70) */
+  double eta;               /* Jacobi damping in (0, 1] */
+  double eps;               /* convergence tolerance relative to mean cost */
+  int max_sweeps;
+  int mode;                 /* 0 = Jacobi, 1 = Gauss-Seidel */
+  int update;               /* 0 = midpoint, 1 = paper-difference */
+  int init;                 /* 0 = local-midpoint, 1 = zero */
+  int threads;              /* accepted for API parity; the device decides its own grid */
+} f2m_engine_config;
+
+typedef struct {            /* ConvergenceReport, dual.hpp:48-54 */
+  int converged;
+  int sweeps;
+  double final_max_abs_delta;
+  double dual_value;
+  double wall_time;
+} f2m_convergence_report;
+
+/* EngineConfig::validate (dual.cpp:13-18) plus the b <= 8 bound the reference forgets. */
+int f2m_engine_config_validate(const f2m_engine_config* cfg);
+
+/* make_initial_state (dual.cpp:194-208): the in-index-order local-midpoint pass (each node
+ * sees the already-updated multipliers of lower-numbered neighbours) or zeros. */
+int f2m_initial_state(const f2m_graph* g, const f2m_engine_config* cfg, double* lambda_out);
+
+/* `count` Jacobi sweeps (jacobi_sweep, dual.cpp:129-167) from lambda_inout, in place.
+ * max_abs_delta[count] (nullable) receives each sweep's max |delta|; dual_value (nullable)
+ * g(lambda) after the last sweep. F2M_E_DEGREE if some degree <= b. */
+int f2m_jacobi_sweeps(const f2m_graph* g, const f2m_engine_config* cfg, double* lambda_inout,
+                      int count, double* max_abs_delta, double* dual_value);
+
+/* `count` Gauss-Seidel sweeps (gauss_seidel_sweep, dual.cpp:175-192), in place. */
+int f2m_gauss_seidel_sweeps(const f2m_graph* g, const f2m_engine_config* cfg,
+                            double* lambda_inout, int count, double* max_abs_delta,
+                            double* dual_value);
+
+/* dual_objective (dual.cpp:87-127): b*sum(lambda) + sum_e min(0, v_e), summed in the
+ * reference's 2048-node / 8192-edge chunk order — bit-exact. */
+int f2m_dual_objective(const f2m_graph* g, const double* lambda, int b, double* out);
+
+/* node_update_delta (dual.cpp:74-85). */
+int f2m_node_update_delta(const f2m_graph* g, const double* lambda, int v, int b, double* out);
+
+/* solve_duals (dual.cpp:210-246): one persistent sm_100a kernel runs every sweep with a
+ * device-side convergence test (max|delta| <= eps*mean_cost); no per-sweep host sync.
+ * lambda_init may be NULL (then cfg->init decides). */
+int f2m_solve_duals(const f2m_graph* g, const f2m_engine_config* cfg, const double* lambda_init,
+                    double* lambda_out, f2m_convergence_report* report);
+
+/* ---- extraction + certificate (primal.hpp) -------------------------------------------- */
+/* classify_edges (primal.cpp:43-63): 0 = NEG, 1 = ZERO, 2 = POS per edge. */
+int f2m_classify_edges(const f2m_graph* g, const double* lambda, double tol, uint8_t* label);
+
+/* extract_primal (primal.cpp:142-233): x[m] in {0, 1/2, 1} and the objective (sequential
+ * sum in edge order, bit-exact). F2M_E_DEGENERATE on the reference's degenerate cases. */
+int f2m_extract_primal(const f2m_graph* g, const double* lambda, double tol, double* x,
+                       double* objective);
+
+/* solve_zero_component (primal.cpp:65-140) — exposed for tests like the reference. */
+int f2m_solve_zero_component(const f2m_graph* g, const int32_t* component_edges, int count,
+                             const int32_t* residual, double* values, int* feasible);
+
+typedef struct {            /* VerificationReport, primal.hpp:25-30 */
+  int feasible;
+  int64_t violated_count;
+  int64_t value_violation_count;
+  double duality_gap;
+} f2m_verification;
+
+/* verify_solution (primal.cpp:235-276). violated_nodes/violated_sums/value_violations may
+ * be NULL; otherwise they receive up to `capacity` entries in node / edge order. */
+int f2m_verify_solution(const f2m_graph* g, const double* x, double objective,
+                        const double* lambda, f2m_verification* report, int32_t* violated_nodes,
+                        double* violated_sums, int32_t* value_violations, int64_t capacity);
+
+/* ---- pipeline (solve.hpp) ------------------------------------------------------------- */
+typedef struct {            /* RunConfig, solve.hpp:15-27 */
+  int k;
+  f2m_engine_config engine;
+  double tol;
+  double gap_tol;
+  int max_restarts;
+  double perturb_scale;
+  uint64_t seed;
+} f2m_run_config;
+
+int f2m_run_config_validate(const f2m_run_config* rc);
+
+typedef struct {            /* SolveOutcome, solve.hpp:29-35 */
+  double objective;
+  f2m_verification verification;
+  f2m_convergence_report convergence;
+  int restarts;
+  /* stage timings (seconds, device events) — observability beyond the reference */
+  double t_knn, t_duals, t_extract, t_total;
+} f2m_solve_outcome;
+
+/* full_solve_graph (solve.cpp:51-99): validate, then restart loop of solve_duals ->
+ * extract_primal -> objective on the original costs -> verify_solution -> certify
+ * (gap <= gap_tol*(1+|obj|)), jittering on the device between attempts.
+ * x (m, nullable) and lambda (n, nullable) are host outputs. F2M_E_SOLVE_FAILED when the
+ * restarts are exhausted. */
+int f2m_full_solve_graph(const f2m_graph* g, const f2m_run_config* rc, double* x,
+                         double* lambda, f2m_solve_outcome* out);
+
+/* full_solve (solve.cpp:101-106): k-NN build with k = max(3, min(k, n-1)) + the above.
+ * `graph_out` (nullable) receives the built graph (caller destroys). */
+int f2m_full_solve(int n, const double* xy, int rounded, const f2m_run_config* rc, double* x,
+                   double* lambda, f2m_solve_outcome* out, f2m_graph** graph_out);
+
+/* Device-resident variant for benchmarking with inputs already in HBM: d_xy (2n doubles)
+ * on the device, d_x (m) / d_lambda (n) device outputs (nullable). */
+int f2m_full_solve_device(int n, const double* d_xy, int rounded, const f2m_run_config* rc,
+                          double* d_x, int64_t d_x_capacity, double* d_lambda,
+                          f2m_solve_outcome* out, f2m_graph** graph_out);
+
+/* ---- instrumentation (bench.py / tests) ----------------------------------------------- */
+/* Number of kernels this library launched since load (all entry points). */
+uint64_t f2m_kernel_launch_count(void);
+/* Device time (ms, CUDA events on the launching stream) of the most recent persistent
+ * sweep kernel and the sweeps it ran. */
+int f2m_last_sweep_kernel_ms(double* ms, int* sweeps);
+/* Algorithmic bytes per sweep of this graph's GDP kernel:
+ * 4(n+1) + 2m*(4+8) + 16n. */
+double f2m_sweep_algorithmic_bytes(const f2m_graph* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* F2M_GPU_H */

@@ -1,0 +1,633 @@
+// core.cu — device/graph plumbing of libf2m_gpu.so: errors, graph creation
+// (Graph::from_edges graph.cpp:14-51, with_costs :53-65, jittered solve.cpp:39-47),
+// the SELL-32 sweep layout, mean cost, validate_graph (graph.cpp:242-277).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <mutex>
+
+#include "internal.cuh"
+
+namespace f2mgpu {
+
+std::atomic<uint64_t> g_launches{0};
+
+static thread_local std::string t_last_error;
+static thread_local int t_device = 0;
+
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+int current_device() { return t_device; }
+
+const cudaDeviceProp& device_props(int dev) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<cudaDeviceProp>> cache(64);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) throw Error(F2M_E_ARGUMENT, "device index out of range");
+  if (!cache[dev]) {
+    auto p = std::make_unique<cudaDeviceProp>();
+    F2M_CUDA(cudaGetDeviceProperties(p.get(), dev));
+    cache[dev] = std::move(p);
+  }
+  return *cache[dev];
+}
+
+Topology::~Topology() {
+  if (stream) {
+    cudaSetDevice(dev);
+    eu.release(); ev.release(); perm.release(); iperm.release(); deg.release();
+    sptr.release(); swidth.release(); scol.release(); seid.release(); cta_lo.release();
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+std::shared_ptr<Topology> make_topology(int n, int dev) {
+  auto t = std::make_shared<Topology>();
+  t->dev = dev;
+  t->n = n;
+  F2M_CUDA(cudaSetDevice(dev));
+  F2M_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  return t;
+}
+
+// ---------------------------------------------------------------- kernels
+
+__global__ void k_edge_keys(int64_t m, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
+                            uint64_t* __restrict__ keys, int64_t* __restrict__ idx) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t a = (uint32_t)min(u[e], v[e]), b = (uint32_t)max(u[e], v[e]);
+  keys[e] = ((uint64_t)a << 32) | b;
+  idx[e] = e;
+}
+
+__global__ void k_unpack_edges(int64_t m, const uint64_t* __restrict__ keys,
+                               const int64_t* __restrict__ idx, const double* __restrict__ cin,
+                               int32_t* __restrict__ u, int32_t* __restrict__ v,
+                               double* __restrict__ cout) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  u[e] = (int32_t)(keys[e] >> 32);
+  v[e] = (int32_t)(keys[e] & 0xffffffffu);
+  cout[e] = cin[idx[e]];
+}
+
+__global__ void k_iota(int n, int32_t* __restrict__ a, int32_t* __restrict__ b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { a[i] = i; b[i] = i; }
+}
+
+// Degree by position: self-loops count once (graph.cpp:30-31).
+__global__ void k_degrees(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                          const int32_t* __restrict__ perm, int32_t* __restrict__ deg) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  atomicAdd(&deg[perm[eu[e]]], 1);
+  if (ev[e] != eu[e]) atomicAdd(&deg[perm[ev[e]]], 1);
+}
+
+// Slice widths (max degree over the 32 positions of a slice) and slice sizes.
+__global__ void k_slice_width(int n, int64_t nslices, const int32_t* __restrict__ deg,
+                              int32_t* __restrict__ width, int64_t* __restrict__ size) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  int w = 0;
+  const int64_t p0 = s * 32;
+  for (int l = 0; l < 32; ++l) {
+    const int64_t p = p0 + l;
+    if (p < n) w = max(w, deg[p]);
+  }
+  width[s] = w;
+  size[s] = (int64_t)w * 32;
+}
+
+__global__ void k_fill_pad(int64_t nslices, const int64_t* __restrict__ sptr,
+                           int32_t* __restrict__ scol, int32_t* __restrict__ seid) {
+  // one warp per slice: padding col = own position, eid = -1
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  for (int64_t t = sptr[s] + lane; t < sptr[s + 1]; t += 32) {
+    scol[t] = (int32_t)(s * 32 + lane);
+    seid[t] = -1;
+  }
+}
+
+__global__ void k_fill_sell(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                            const int32_t* __restrict__ perm, const int64_t* __restrict__ sptr,
+                            int32_t* __restrict__ fill, int32_t* __restrict__ scol,
+                            int32_t* __restrict__ seid) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const int pu = perm[eu[e]], pv = perm[ev[e]];
+  {
+    const int j = atomicAdd(&fill[pu], 1);
+    const int64_t t = sptr[pu >> 5] + (int64_t)j * 32 + (pu & 31);
+    scol[t] = pv;
+    seid[t] = (int32_t)e;
+  }
+  if (pu != pv) {
+    const int j = atomicAdd(&fill[pv], 1);
+    const int64_t t = sptr[pv >> 5] + (int64_t)j * 32 + (pv & 31);
+    scol[t] = pu;
+    seid[t] = (int32_t)e;
+  }
+}
+
+// CTA partition of slices balanced by padded slot count: cta_lo[c] = first slice whose
+// start offset is >= c * total / ctas.
+__global__ void k_partition(int ctas, int64_t nslices, const int64_t* __restrict__ sptr,
+                            int32_t* __restrict__ lo) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > ctas) return;
+  if (c == ctas) { lo[c] = (int32_t)nslices; return; }
+  const int64_t total = sptr[nslices];
+  // target in slots, mixed with a per-slice fixed cost so empty-ish slices still spread
+  const double target = (double)c / ctas;
+  int64_t a = 0, b = nslices;
+  while (a < b) {
+    const int64_t mid = (a + b) / 2;
+    const double f = ((double)sptr[mid] + 64.0 * mid) / ((double)total + 64.0 * nslices);
+    if (f < target) a = mid + 1; else b = mid;
+  }
+  lo[c] = (int32_t)a;
+}
+
+__global__ void k_scost(int64_t slots, const int32_t* __restrict__ seid,
+                        const double* __restrict__ cost, double* __restrict__ scost) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= slots) return;
+  const int32_t e = seid[t];
+  scost[t] = e >= 0 ? cost[e] : CUDART_INF;
+}
+
+// Graph::from_edges mean (graph.cpp:47-49): a SEQUENTIAL fp64 sum in edge order. It sets the
+// convergence threshold eps*mean_cost, so it must be bit-exact: one block stages coalesced
+// tiles in shared memory and a single thread adds them in order.
+__global__ void __launch_bounds__(256) k_sequential_mean(int64_t m, const double* __restrict__ c,
+                                                         double* __restrict__ out) {
+  __shared__ double tile[2][1024];
+  double acc = 0.0;
+  const int64_t ntiles = (m + 1023) / 1024;
+  if (ntiles > 0) {
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) tile[0][i] = i < m ? c[i] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < ntiles) {  // prefetch the next tile while thread 0 sums this one
+      const int64_t base = (t + 1) * 1024;
+      for (int i = threadIdx.x; i < 1024; i += blockDim.x)
+        tile[cur ^ 1][i] = base + i < m ? c[base + i] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+      const int cnt = (int)min64(1024, m - t * 1024);
+      for (int i = 0; i < cnt; ++i) acc = dadd(acc, tile[cur][i]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = m > 0 ? __ddiv_rn(acc, (double)m) : 0.0;
+}
+
+__global__ void k_jitter(int64_t m, const double* __restrict__ cin, double amplitude,
+                         uint64_t state0, double* __restrict__ cout) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  // graph.edge(e).cost + amplitude * rng.next_double()  (solve.cpp:44), no contraction
+  cout[e] = dadd(cin[e], dmul(amplitude, splitmix64_double_at(state0, (uint64_t)e)));
+}
+
+// validate_graph edge checks (graph.cpp:245-263): first offending edge in edge order.
+__global__ void k_validate(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                           const double* __restrict__ cost, unsigned long long* __restrict__ first) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  int kind = 0;
+  if (eu[e] == ev[e]) kind = 1;                                        // self-loop
+  else if (e > 0 && eu[e - 1] == eu[e] && ev[e - 1] == ev[e]) kind = 2; // duplicate
+  else if (!(cost[e] >= 0.0)) kind = 3;                                // negative cost
+  if (kind) atomicMin(first, ((unsigned long long)e << 2) | (unsigned long long)kind);
+}
+
+__global__ void k_minmax_deg(int n, const int32_t* __restrict__ deg, int* __restrict__ mn,
+                             int* __restrict__ mx) {
+  int lo = INT_MAX, hi = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    lo = min(lo, deg[i]);
+    hi = max(hi, deg[i]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mn, lo);
+    atomicMax(mx, hi);
+  }
+}
+
+__global__ void k_gather_i32(int n, const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
+                             int32_t* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void k_gather_f64(int n, const double* __restrict__ src, const int32_t* __restrict__ idx,
+                             double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void k_scatter_f64(int n, const double* __restrict__ src, const int32_t* __restrict__ idx,
+                              double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+}
+
+__global__ void k_incidence_keys(int64_t m, const int32_t* __restrict__ eu,
+                                 const int32_t* __restrict__ ev, const int64_t* __restrict__ off,
+                                 int32_t* __restrict__ cur, int32_t* __restrict__ ids) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  ids[off[eu[e]] + atomicAdd(&cur[eu[e]], 1)] = (int32_t)e;
+  if (ev[e] != eu[e]) ids[off[ev[e]] + atomicAdd(&cur[ev[e]], 1)] = (int32_t)e;
+}
+
+// ---------------------------------------------------------------- host helpers
+
+void sort_edges(Topology& t, DBuf<int32_t>& eu, DBuf<int32_t>& ev, DBuf<double>& cost) {
+  const int64_t m = t.m;
+  cudaStream_t s = t.stream;
+  DBuf<uint64_t> k0(m, s), k1(m, s);
+  DBuf<int64_t> i0(m, s), i1(m, s);
+  if (m > 0) {
+    k_edge_keys<<<grid_for(m, 256), 256, 0, s>>>(m, eu.get(), ev.get(), k0.get(), i0.get());
+    launched("edge_keys");
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.get(), k1.get(), i0.get(), i1.get(),
+                                             m, 0, 64, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceRadixSort::SortPairs(tb.get(), tmp, k0.get(), k1.get(), i0.get(), i1.get(),
+                                             m, 0, 64, s));
+    launched("radix_sort_edges");
+  }
+  t.eu.alloc(m, s);
+  t.ev.alloc(m, s);
+  DBuf<double> c2(m, s);
+  if (m > 0) {
+    k_unpack_edges<<<grid_for(m, 256), 256, 0, s>>>(m, k1.get(), i1.get(), cost.get(), t.eu.get(),
+                                                   t.ev.get(), c2.get());
+    launched("unpack_edges");
+  }
+  cost = std::move(c2);
+}
+
+void identity_perm(Topology& t) {
+  t.perm.alloc(t.n, t.stream);
+  t.iperm.alloc(t.n, t.stream);
+  if (t.n > 0) {
+    k_iota<<<grid_for(t.n, 256), 256, 0, t.stream>>>(t.n, t.perm.get(), t.iperm.get());
+    launched("iota");
+  }
+}
+
+void finalize_topology(Topology& t) {
+  cudaStream_t s = t.stream;
+  const int n = t.n;
+  const int64_t m = t.m;
+  t.deg.alloc(n, s);
+  if (n > 0) F2M_CUDA(cudaMemsetAsync(t.deg.get(), 0, sizeof(int32_t) * n, s));
+  if (m > 0) {
+    k_degrees<<<grid_for(m, 256), 256, 0, s>>>(m, t.eu.get(), t.ev.get(), t.perm.get(), t.deg.get());
+    launched("degrees");
+  }
+  // min / max degree
+  {
+    DBuf<int> mm(2, s);
+    int init[2] = {n > 0 ? INT_MAX : 0, 0};
+    F2M_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+    if (n > 0) {
+      k_minmax_deg<<<std::min<unsigned>(grid_for(n, 256), 1184), 256, 0, s>>>(n, t.deg.get(),
+                                                                               mm.get(), mm.get() + 1);
+      launched("minmax_deg");
+    }
+    int out[2];
+    F2M_CUDA(cudaMemcpyAsync(out, mm.get(), sizeof(out), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    t.min_deg = out[0];
+    t.max_deg = out[1];
+  }
+  // SELL-32 layout
+  t.nslices = (n + 31) / 32;
+  t.swidth.alloc(t.nslices, s);
+  t.sptr.alloc(t.nslices + 1, s);
+  DBuf<int64_t> ssize(t.nslices + 1, s);
+  if (t.nslices > 0) {
+    k_slice_width<<<grid_for(t.nslices, 256), 256, 0, s>>>(n, t.nslices, t.deg.get(), t.swidth.get(),
+                                                          ssize.get());
+    launched("slice_width");
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ssize.get(), t.sptr.get(), t.nslices + 1, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, ssize.get(), t.sptr.get(), t.nslices + 1, s));
+    launched("scan_slices");
+  } else {
+    F2M_CUDA(cudaMemsetAsync(t.sptr.get(), 0, sizeof(int64_t), s));
+  }
+  // exclusive scan over nslices+1 entries: sptr[nslices] = total padded slots (the last
+  // input entry never contributes to an exclusive sum)
+  int64_t slots = 0;
+  F2M_CUDA(cudaMemcpyAsync(&slots, t.sptr.get() + t.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  F2M_CUDA(cudaStreamSynchronize(s));
+  t.sell_slots = slots;
+  t.scol.alloc(slots, s);
+  t.seid.alloc(slots, s);
+  if (t.nslices > 0) {
+    k_fill_pad<<<grid_for(t.nslices * 32, 256), 256, 0, s>>>(t.nslices, t.sptr.get(), t.scol.get(),
+                                                            t.seid.get());
+    launched("fill_pad");
+  }
+  if (m > 0) {
+    DBuf<int32_t> fill(n, s);
+    F2M_CUDA(cudaMemsetAsync(fill.get(), 0, sizeof(int32_t) * n, s));
+    k_fill_sell<<<grid_for(m, 256), 256, 0, s>>>(m, t.eu.get(), t.ev.get(), t.perm.get(), t.sptr.get(),
+                                                fill.get(), t.scol.get(), t.seid.get());
+    launched("fill_sell");
+  }
+  // persistent-sweep CTA partition
+  t.sweep_ctas = sweep_grid_ctas(t.dev);
+  t.cta_lo.alloc(t.sweep_ctas + 1, s);
+  k_partition<<<grid_for(t.sweep_ctas + 1, 128), 128, 0, s>>>(t.sweep_ctas, t.nslices, t.sptr.get(),
+                                                              t.cta_lo.get());
+  launched("partition");
+}
+
+double sequential_mean(const double* d_cost, int64_t m, cudaStream_t s) {
+  DBuf<double> out(1, s);
+  k_sequential_mean<<<1, 256, 0, s>>>(m, d_cost, out.get());
+  launched("sequential_mean");
+  double h = 0.0;
+  F2M_CUDA(cudaMemcpyAsync(&h, out.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  F2M_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+void attach_costs(f2m_graph& g) {
+  Topology& t = *g.topo;
+  g.scost.alloc(t.sell_slots, t.stream);
+  if (t.sell_slots > 0) {
+    k_scost<<<grid_for(t.sell_slots, 256), 256, 0, t.stream>>>(t.sell_slots, t.seid.get(),
+                                                               g.cost.get(), g.scost.get());
+    launched("scost");
+  }
+  g.mean_cost = sequential_mean(g.cost.get(), t.m, t.stream);
+}
+
+void upload_lambda(const f2m_graph& g, const double* h_lambda, double* d_lam_pos) {
+  const Topology& t = *g.topo;
+  if (t.n == 0) return;
+  DBuf<double> tmp(t.n, t.stream);
+  F2M_CUDA(cudaMemcpyAsync(tmp.get(), h_lambda, sizeof(double) * t.n, cudaMemcpyHostToDevice, t.stream));
+  k_scatter_f64<<<grid_for(t.n, 256), 256, 0, t.stream>>>(t.n, tmp.get(), t.perm.get(), d_lam_pos);
+  launched("scatter_lambda");
+}
+
+void download_lambda(const f2m_graph& g, const double* d_lam_pos, double* h_lambda) {
+  const Topology& t = *g.topo;
+  if (t.n == 0) return;
+  DBuf<double> tmp(t.n, t.stream);
+  k_gather_f64<<<grid_for(t.n, 256), 256, 0, t.stream>>>(t.n, d_lam_pos, t.perm.get(), tmp.get());
+  launched("gather_lambda");
+  F2M_CUDA(cudaMemcpyAsync(h_lambda, tmp.get(), sizeof(double) * t.n, cudaMemcpyDeviceToHost, t.stream));
+  F2M_CUDA(cudaStreamSynchronize(t.stream));
+}
+
+}  // namespace f2mgpu
+
+using namespace f2mgpu;
+
+// ====================================================================== C ABI
+
+extern "C" const char* f2m_last_error(void) { return t_last_error.c_str(); }
+
+extern "C" int f2m_set_device(int device) {
+  return guard([&] {
+    int count = 0;
+    F2M_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw Error(F2M_E_ARGUMENT, "f2m_set_device: no such device");
+    F2M_CUDA(cudaSetDevice(device));
+    t_device = device;
+  });
+}
+
+extern "C" int f2m_get_device_info(f2m_device_info* out) {
+  return guard([&] {
+    const int dev = current_device();
+    F2M_CUDA(cudaSetDevice(dev));
+    const cudaDeviceProp& p = device_props(dev);
+    out->device = dev;
+    out->sm_count = p.multiProcessorCount;
+    out->sweep_ctas = sweep_grid_ctas(dev);
+    out->sweep_threads = sweep_block_threads();
+    out->cc_major = p.major;
+    out->cc_minor = p.minor;
+    std::snprintf(out->name, sizeof(out->name), "%s", p.name);
+  });
+}
+
+extern "C" uint64_t f2m_kernel_launch_count(void) { return g_launches.load(); }
+
+extern "C" int f2m_graph_from_edges(int n, int64_t m, const int32_t* eu, const int32_t* ev,
+                                    const double* cost, f2m_graph** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (n < 0) throw Error(F2M_E_ARGUMENT, "from_edges: negative node count");
+    if (m < 0) throw Error(F2M_E_ARGUMENT, "from_edges: negative edge count");
+    if (m >= (int64_t(1) << 30)) throw Error(F2M_E_ARGUMENT, "from_edges: too many edges");
+    for (int64_t e = 0; e < m; ++e) {  // graph.cpp:16-19: IndexError before anything else
+      if (eu[e] < 0 || eu[e] >= n || ev[e] < 0 || ev[e] >= n)
+        throw Error(F2M_E_INDEX, "edge endpoint out of range");
+    }
+    const int dev = current_device();
+    F2M_CUDA(cudaSetDevice(dev));
+    auto g = std::make_unique<f2m_graph>();
+    g->topo = make_topology(n, dev);
+    Topology& t = *g->topo;
+    t.m = m;
+    cudaStream_t s = t.stream;
+    DBuf<int32_t> du(m, s), dv(m, s);
+    g->cost.alloc(m, s);
+    if (m > 0) {
+      F2M_CUDA(cudaMemcpyAsync(du.get(), eu, sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+      F2M_CUDA(cudaMemcpyAsync(dv.get(), ev, sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+      F2M_CUDA(cudaMemcpyAsync(g->cost.get(), cost, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    }
+    sort_edges(t, du, dv, g->cost);
+    identity_perm(t);
+    finalize_topology(t);
+    attach_costs(*g);
+    F2M_CUDA(cudaStreamSynchronize(s));
+    *out = g.release();
+  });
+}
+
+extern "C" int f2m_graph_with_costs(const f2m_graph* g, const double* cost, f2m_graph** out) {
+  return guard([&] {
+    *out = nullptr;
+    F2M_CUDA(cudaSetDevice(g->topo->dev));
+    auto h = std::make_unique<f2m_graph>();
+    h->topo = g->topo;
+    const Topology& t = *h->topo;
+    h->cost.alloc(t.m, t.stream);
+    if (t.m > 0)
+      F2M_CUDA(cudaMemcpyAsync(h->cost.get(), cost, sizeof(double) * t.m, cudaMemcpyHostToDevice, t.stream));
+    attach_costs(*h);
+    *out = h.release();
+  });
+}
+
+extern "C" int f2m_graph_jittered(const f2m_graph* g, uint64_t seed, int restart,
+                                  double perturb_scale, f2m_graph** out) {
+  return guard([&] {
+    *out = nullptr;
+    F2M_CUDA(cudaSetDevice(g->topo->dev));
+    auto h = std::make_unique<f2m_graph>();
+    h->topo = g->topo;
+    const Topology& t = *h->topo;
+    // cost_scale (solve.cpp:33-35) and amplitude (:40) are host scalars, as in the reference
+    const double scale = g->mean_cost > 0.0 ? g->mean_cost : 1.0;
+    const double amplitude = perturb_scale * scale;
+    const uint64_t state0 = seed * 0x9E3779B97F4A7C15ULL + static_cast<uint64_t>(restart);
+    h->cost.alloc(t.m, t.stream);
+    if (t.m > 0) {
+      k_jitter<<<grid_for(t.m, 256), 256, 0, t.stream>>>(t.m, g->cost.get(), amplitude, state0,
+                                                        h->cost.get());
+      launched("jitter");
+    }
+    attach_costs(*h);
+    *out = h.release();
+  });
+}
+
+extern "C" void f2m_graph_destroy(f2m_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->topo->dev);
+  delete g;
+}
+
+extern "C" int f2m_graph_get_info(const f2m_graph* g, f2m_graph_info* out) {
+  return guard([&] {
+    const Topology& t = *g->topo;
+    out->n = t.n;
+    out->m = t.m;
+    out->mean_cost = g->mean_cost;
+    out->min_degree = t.min_deg;
+    out->max_degree = t.max_deg;
+    out->sell_slots = t.sell_slots;
+  });
+}
+
+extern "C" int f2m_graph_edges(const f2m_graph* g, int32_t* eu, int32_t* ev, double* cost) {
+  return guard([&] {
+    const Topology& t = *g->topo;
+    F2M_CUDA(cudaSetDevice(t.dev));
+    if (t.m > 0) {
+      if (eu) F2M_CUDA(cudaMemcpyAsync(eu, t.eu.get(), sizeof(int32_t) * t.m, cudaMemcpyDeviceToHost, t.stream));
+      if (ev) F2M_CUDA(cudaMemcpyAsync(ev, t.ev.get(), sizeof(int32_t) * t.m, cudaMemcpyDeviceToHost, t.stream));
+      if (cost) F2M_CUDA(cudaMemcpyAsync(cost, g->cost.get(), sizeof(double) * t.m, cudaMemcpyDeviceToHost, t.stream));
+    }
+    F2M_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+extern "C" int f2m_graph_degrees(const f2m_graph* g, int32_t* degree) {
+  return guard([&] {
+    const Topology& t = *g->topo;
+    F2M_CUDA(cudaSetDevice(t.dev));
+    if (t.n == 0) return;
+    DBuf<int32_t> tmp(t.n, t.stream);
+    k_gather_i32<<<grid_for(t.n, 256), 256, 0, t.stream>>>(t.n, t.deg.get(), t.perm.get(), tmp.get());
+    launched("gather_deg");
+    F2M_CUDA(cudaMemcpyAsync(degree, tmp.get(), sizeof(int32_t) * t.n, cudaMemcpyDeviceToHost, t.stream));
+    F2M_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+extern "C" int f2m_graph_incidence(const f2m_graph* g, int64_t* offsets, int32_t* ids) {
+  return guard([&] {
+    const Topology& t = *g->topo;
+    F2M_CUDA(cudaSetDevice(t.dev));
+    cudaStream_t s = t.stream;
+    const int n = t.n;
+    const int64_t m = t.m;
+    DBuf<int32_t> deg(n, s);
+    DBuf<int64_t> degl(n + 1, s), off(n + 1, s);
+    if (n > 0) {
+      k_gather_i32<<<grid_for(n, 256), 256, 0, s>>>(n, t.deg.get(), t.perm.get(), deg.get());
+      launched("gather_deg");
+    }
+    std::vector<int32_t> hdeg(n);
+    if (n > 0)
+      F2M_CUDA(cudaMemcpyAsync(hdeg.data(), deg.get(), sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    offsets[0] = 0;
+    for (int v = 0; v < n; ++v) offsets[v + 1] = offsets[v] + hdeg[v];
+    const int64_t slots = offsets[n];
+    DBuf<int32_t> d_ids(slots, s), cur(n, s);
+    if (n > 0) {
+      F2M_CUDA(cudaMemcpyAsync(off.get(), offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+      F2M_CUDA(cudaMemsetAsync(cur.get(), 0, sizeof(int32_t) * n, s));
+    }
+    if (m > 0) {
+      k_incidence_keys<<<grid_for(m, 256), 256, 0, s>>>(m, t.eu.get(), t.ev.get(), off.get(), cur.get(),
+                                                       d_ids.get());
+      launched("incidence");
+    }
+    if (slots > 0)
+      F2M_CUDA(cudaMemcpyAsync(ids, d_ids.get(), sizeof(int32_t) * slots, cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    // rows hold ascending edge ids in the reference (graph.cpp:38-44)
+    for (int v = 0; v < n; ++v) std::sort(ids + offsets[v], ids + offsets[v + 1]);
+  });
+}
+
+extern "C" int f2m_graph_validate(const f2m_graph* g, int* min_degree, int* max_degree,
+                                  int64_t* edges) {
+  return guard([&] {
+    const Topology& t = *g->topo;
+    F2M_CUDA(cudaSetDevice(t.dev));
+    cudaStream_t s = t.stream;
+    if (t.m > 0) {
+      DBuf<unsigned long long> first(1, s);
+      F2M_CUDA(cudaMemsetAsync(first.get(), 0xff, sizeof(unsigned long long), s));
+      k_validate<<<grid_for(t.m, 256), 256, 0, s>>>(t.m, t.eu.get(), t.ev.get(), g->cost.get(), first.get());
+      launched("validate");
+      unsigned long long h = 0;
+      F2M_CUDA(cudaMemcpyAsync(&h, first.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+      F2M_CUDA(cudaStreamSynchronize(s));
+      if (h != ~0ULL) {
+        const int64_t e = (int64_t)(h >> 2);
+        const int kind = (int)(h & 3);
+        int32_t u = 0, v = 0;
+        F2M_CUDA(cudaMemcpy(&u, t.eu.get() + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        F2M_CUDA(cudaMemcpy(&v, t.ev.get() + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (kind == 1) throw Error(F2M_E_STRUCTURE, "self-loop at node " + std::to_string(u));
+        if (kind == 2)
+          throw Error(F2M_E_STRUCTURE, "duplicate edge (" + std::to_string(u) + ", " + std::to_string(v) + ")");
+        throw Error(F2M_E_STRUCTURE,
+                    "negative cost on edge (" + std::to_string(u) + ", " + std::to_string(v) + ")");
+      }
+    }
+    const int mn = t.n > 0 ? t.min_deg : 0;
+    if (min_degree) *min_degree = mn;
+    if (max_degree) *max_degree = t.max_deg;
+    if (edges) *edges = t.m;
+    if (mn < 3)
+      throw Error(F2M_E_MIN_DEGREE, "node degree " + std::to_string(mn) +
+                                        " below 3; the node update needs a third-shortest edge");
+  });
+}
+
+extern "C" double f2m_sweep_algorithmic_bytes(const f2m_graph* g) {
+  const Topology& t = *g->topo;
+  return 4.0 * (t.n + 1) + 2.0 * t.m * 12.0 + 16.0 * t.n;
+}

@@ -1,0 +1,249 @@
+// internal.cuh — shared internals of libf2m_gpu.so (sm_100a).
+//
+// Device data layout:
+//   edge list   eu/ev int32[m], cost fp64[m]      reference edge order: (u, v) sorted, u < v
+//   perm/iperm  int32[n]                          node id <-> device position (Morton order of
+//                                                 the k-NN grid cells; identity for from_edges)
+//   SELL-32     sptr int64[S+1], swidth int32[S]  slice s = positions 32s..32s+31; slot j of
+//               scol int32[], scost fp64[]        position p lives at sptr[s] + 32*j + (p&31):
+//               seid int32[]                      one coalesced 128 B col / 256 B cost line per
+//                                                 warp per j. Padding: col = p, cost = +inf,
+//                                                 eid = -1 (never selected: inf < s_b is false).
+//   lambda      fp64[n] in position order, double buffered by the sweep kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "f2m_gpu.h"
+
+namespace f2mgpu {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define F2M_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      throw ::f2mgpu::Error(e_ == cudaErrorMemoryAllocation ? F2M_E_NOMEM : F2M_E_CUDA,   \
+                            std::string("CUDA error ") + cudaGetErrorString(e_) + " at " + \
+                                __FILE__ + ":" + std::to_string(__LINE__));               \
+    }                                                                                     \
+  } while (0)
+
+// Wraps a C-ABI body: converts exceptions to status codes + thread-local message.
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return F2M_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failure");
+    return F2M_E_NOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return F2M_E_CUDA;
+  }
+}
+
+// Kernel launch accounting (f2m_kernel_launch_count) + launch error check.
+extern std::atomic<uint64_t> g_launches;
+inline void launched(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    throw Error(F2M_E_CUDA, std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
+  }
+}
+
+int current_device();
+const cudaDeviceProp& device_props(int dev);
+
+// ---------------------------------------------------------------- device buffers
+// Stream-ordered allocation (cudaMallocAsync) so scratch reuse is cheap.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) F2M_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---------------------------------------------------------------- graph structures
+struct Topology {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int n = 0;
+  int64_t m = 0;
+  DBuf<int32_t> eu, ev;        // [m] sorted (u, v), u <= v (self-loops kept)
+  DBuf<int32_t> perm, iperm;   // [n]
+  DBuf<int32_t> deg;           // [n] by position
+  int64_t nslices = 0;
+  int64_t sell_slots = 0;
+  DBuf<int64_t> sptr;          // [nslices+1]
+  DBuf<int32_t> swidth;        // [nslices]
+  DBuf<int32_t> scol;          // [sell_slots]
+  DBuf<int32_t> seid;          // [sell_slots]
+  int min_deg = 0, max_deg = 0;
+  // persistent-sweep partition: CTA c owns slices [cta_lo[c], cta_lo[c+1])
+  int sweep_ctas = 0;
+  DBuf<int32_t> cta_lo;        // [sweep_ctas+1]
+  ~Topology();
+};
+
+}  // namespace f2mgpu
+
+struct f2m_graph {
+  std::shared_ptr<f2mgpu::Topology> topo;
+  f2mgpu::DBuf<double> cost;   // [m] reference edge order
+  f2mgpu::DBuf<double> scost;  // [sell_slots] per SELL slot (+inf on padding)
+  double mean_cost = 0.0;
+};
+
+namespace f2mgpu {
+
+constexpr int kMaxB = 8;          // dual.cpp:70
+constexpr int kNodeChunk = 2048;  // parallel.hpp:15
+constexpr int kEdgeChunk = 8192;  // parallel.hpp:16
+constexpr int kMaxComponentEdges = 20;  // primal.cpp:17
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+inline unsigned grid_for(int64_t items, int block) {
+  int64_t g = (items + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (1 << 30)) g = 1 << 30;
+  return static_cast<unsigned>(g);
+}
+
+// Shared building blocks (core.cu)
+std::shared_ptr<Topology> make_topology(int n, int dev);  // owns a fresh non-blocking stream
+// Sorts + normalizes device edges in place into eu/ev/cost (stable by (u,v)).
+void sort_edges(Topology& t, DBuf<int32_t>& eu, DBuf<int32_t>& ev, DBuf<double>& cost);
+// Builds degrees, SELL-32 layout and the persistent-sweep partition for the given perm.
+void finalize_topology(Topology& t);
+// Identity permutation.
+void identity_perm(Topology& t);
+// cost -> scost, mean_cost (bit-exact sequential sum on the device).
+void attach_costs(f2m_graph& g);
+double sequential_mean(const double* d_cost, int64_t m, cudaStream_t s);
+
+// Lambda layout conversion (host orig order <-> device position order).
+void upload_lambda(const f2m_graph& g, const double* h_lambda, double* d_lam_pos);
+void download_lambda(const f2m_graph& g, const double* d_lam_pos, double* h_lambda);
+
+// dual.cu
+double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b);
+void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam_pos);
+struct SweepResult {
+  int sweeps = 0;
+  int converged = 0;
+  double final_max_abs_delta = INFINITY;
+  int out_buffer = 0;  // which of the two buffers holds the result
+};
+SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam0,
+                       double* d_lam1, int max_sweeps, double threshold, double* d_record);
+void validate_engine(const f2m_engine_config& cfg);
+void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const double* d_init,
+                        DBuf<double>& d_lam_out, f2m_convergence_report& rep);
+
+// primal.cu
+void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, double* d_x);
+double objective_device(const f2m_graph& g, const double* d_x);
+void verify_device(const f2m_graph& g, const double* d_x, double objective,
+                   const double* d_lam_pos, f2m_verification& rep, int32_t* h_nodes,
+                   double* h_sums, int32_t* h_vals, int64_t capacity);
+
+// persistent sweep launch geometry (dual.cu)
+int sweep_grid_ctas(int dev);
+int sweep_block_threads();
+
+// knn.cu
+// xy: device pointer, or host pointer when xy_on_host (staged on the graph's own stream).
+// start (nullable) is recorded on the graph's stream before any work (for device timing).
+f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounded, int k, int dev,
+                            cudaEvent_t start);
+
+// ---------------------------------------------------------------- device helpers
+// IEEE fp64 with no contraction: the reference is compiled without FMA (no -march), so
+// every multiply-add below is an explicit rounded multiply followed by a rounded add.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+__device__ __forceinline__ uint64_t splitmix64_at(uint64_t state0, uint64_t draw_index) {
+  // SplitMix64 (instance.hpp:54-60) is counter-based: the state before draw j (0-based) is
+  // state0 + j*gamma, and next() first adds gamma.
+  uint64_t z = state0 + (draw_index + 1ULL) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double splitmix64_double_at(uint64_t state0, uint64_t j) {
+  return static_cast<double>(splitmix64_at(state0, j) >> 11) * 0x1.0p-53;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace f2mgpu

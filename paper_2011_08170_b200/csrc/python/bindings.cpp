@@ -1,0 +1,412 @@
+// bindings.cpp — pybind11 module `_f2m`: the reference's Python surface
+// (/root/reference/proj/python/bindings.cpp — same function names, keyword arguments, defaults
+// and exception mapping) over the B200 solver, plus numpy/device entry points used by the
+// benchmark and the parity tests.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <sstream>
+
+#include "f2m/api.hpp"
+#include "f2m_gpu.h"
+
+namespace py = pybind11;
+
+namespace {
+
+f2m::EngineConfig engine_config(int b, double eta, double eps, int max_sweeps, const std::string& mode,
+                                const std::string& update, const std::string& init, int threads) {
+  f2m::EngineConfig c;
+  c.b = b;
+  c.eta = eta;
+  c.eps = eps;
+  c.max_sweeps = max_sweeps;
+  c.mode = mode == "gauss-seidel" ? f2m::SweepMode::kGaussSeidel : f2m::SweepMode::kJacobi;
+  c.update = update == "paper-difference" ? f2m::UpdateRule::kPaperDifference : f2m::UpdateRule::kMidpoint;
+  c.init = init == "zero" ? f2m::DualInit::kZero : f2m::DualInit::kLocalMidpoint;
+  c.threads = threads;
+  c.validate();
+  return c;
+}
+
+f2m_run_config run_config_c(int k, double eta, double eps, int max_sweeps, const std::string& mode, double tol,
+                            int max_restarts, std::uint64_t seed, double gap_tol, double perturb_scale) {
+  f2m_run_config rc{};
+  rc.k = k;
+  rc.engine.b = 2;
+  rc.engine.eta = eta;
+  rc.engine.eps = eps;
+  rc.engine.max_sweeps = max_sweeps;
+  rc.engine.mode = mode == "gauss-seidel" ? 1 : 0;
+  rc.tol = tol;
+  rc.gap_tol = gap_tol;
+  rc.max_restarts = max_restarts;
+  rc.perturb_scale = perturb_scale;
+  rc.seed = seed;
+  return rc;
+}
+
+py::dict outcome_dict(const f2m_solve_outcome& o) {
+  return py::dict(py::arg("objective") = o.objective, py::arg("feasible") = o.verification.feasible != 0,
+                  py::arg("gap") = o.verification.duality_gap, py::arg("sweeps") = o.convergence.sweeps,
+                  py::arg("converged") = o.convergence.converged != 0,
+                  py::arg("final_max_abs_delta") = o.convergence.final_max_abs_delta,
+                  py::arg("dual_value") = o.convergence.dual_value, py::arg("restarts") = o.restarts,
+                  py::arg("t_knn") = o.t_knn, py::arg("t_duals") = o.t_duals, py::arg("t_extract") = o.t_extract,
+                  py::arg("t_total") = o.t_total);
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_f2m, m) {
+  m.doc() = "B200-native fractional 2-matching solver (GDP over k-NN graphs, sm_100a)";
+
+  py::register_exception<f2m::ParseError>(m, "ParseError", PyExc_ValueError);
+  py::register_exception<f2m::DegenerateExtraction>(m, "DegenerateExtraction", PyExc_RuntimeError);
+  py::register_exception<f2m::TooLarge>(m, "TooLarge", PyExc_ValueError);
+  py::register_exception<f2m::Infeasible>(m, "Infeasible", PyExc_RuntimeError);
+  py::register_exception<f2m::SolveFailed>(m, "SolveFailed", PyExc_RuntimeError);
+  py::register_exception<f2m::DeviceError>(m, "DeviceError", PyExc_RuntimeError);
+
+  py::enum_<f2m::DistanceMode>(m, "DistanceMode")
+      .value("EUC2D_ROUNDED", f2m::DistanceMode::kEuc2dRounded)
+      .value("EUC2D_EXACT", f2m::DistanceMode::kEuc2dExact);
+
+  py::class_<f2m::Instance>(m, "Instance")
+      .def_readonly("name", &f2m::Instance::name)
+      .def_readwrite("mode", &f2m::Instance::mode)
+      .def_property_readonly("points",
+                             [](const f2m::Instance& inst) {
+                               std::vector<std::pair<double, double>> pts;
+                               pts.reserve(inst.points.size());
+                               for (const auto& p : inst.points) pts.emplace_back(p.x, p.y);
+                               return pts;
+                             })
+      .def("__len__", &f2m::Instance::node_count)
+      .def("distance", [](const f2m::Instance& inst, int i, int j) { return f2m::distance(inst, i, j); })
+      // --- extensions: zero-copy-ish numpy construction and export
+      .def_static(
+          "from_points",
+          [](py::array_t<double, py::array::c_style | py::array::forcecast> xy, f2m::DistanceMode mode,
+             const std::string& name) {
+            if (xy.ndim() != 2 || xy.shape(1) != 2) throw f2m::ArgumentError("from_points: expected an (n, 2) array");
+            f2m::Instance inst;
+            inst.name = name;
+            inst.mode = mode;
+            inst.points.resize(static_cast<size_t>(xy.shape(0)));
+            const double* p = xy.data();
+            for (size_t i = 0; i < inst.points.size(); ++i) inst.points[i] = f2m::Point{p[2 * i], p[2 * i + 1]};
+            return inst;
+          },
+          py::arg("xy"), py::arg("mode") = f2m::DistanceMode::kEuc2dExact, py::arg("name") = "")
+      .def("points_array", [](const f2m::Instance& inst) {
+        py::array_t<double> a({static_cast<py::ssize_t>(inst.points.size()), static_cast<py::ssize_t>(2)});
+        double* p = a.mutable_data();
+        for (size_t i = 0; i < inst.points.size(); ++i) {
+          p[2 * i] = inst.points[i].x;
+          p[2 * i + 1] = inst.points[i].y;
+        }
+        return a;
+      });
+
+  m.def("parse_tsplib", &f2m::parse_tsplib_string, py::arg("text"));
+  m.def("load_tsplib", &f2m::load_tsplib_file, py::arg("path"));
+  m.def(
+      "serialize_tsplib",
+      [](const f2m::Instance& instance) {
+        std::ostringstream out;
+        f2m::serialize_tsplib(instance, out);
+        return out.str();
+      },
+      py::arg("instance"));
+  m.def("generate_instance", &f2m::generate_instance, py::arg("n"), py::arg("seed"), py::arg("box") = 1000.0);
+  m.def("generate_clustered_instance", &f2m::generate_clustered_instance, py::arg("n"), py::arg("seed"),
+        py::arg("box") = 1000.0);
+
+  py::class_<f2m::Graph>(m, "Graph")
+      .def_property_readonly("n", &f2m::Graph::node_count)
+      .def_property_readonly("m", &f2m::Graph::edge_count)
+      .def("edges",
+           [](const f2m::Graph& g) {
+             std::vector<std::tuple<int, int, double>> out;
+             out.reserve(g.edges().size());
+             for (const auto& e : g.edges()) out.emplace_back(e.u, e.v, e.cost);
+             return out;
+           })
+      .def("degree", &f2m::Graph::degree)
+      .def("mean_cost", &f2m::Graph::mean_cost)
+      // --- extensions
+      .def("edge_arrays",
+           [](const f2m::Graph& g) {
+             const py::ssize_t mm = g.edge_count();
+             py::array_t<int32_t> u(mm), v(mm);
+             py::array_t<double> c(mm);
+             if (mm) f2m::check(f2m_graph_edges(g.handle(), u.mutable_data(), v.mutable_data(), c.mutable_data()));
+             return py::make_tuple(u, v, c);
+           })
+      .def("degrees",
+           [](const f2m::Graph& g) {
+             py::array_t<int32_t> d(g.node_count());
+             if (g.node_count()) f2m::check(f2m_graph_degrees(g.handle(), d.mutable_data()));
+             return d;
+           })
+      .def("with_costs", &f2m::Graph::with_costs, py::arg("costs"))
+      .def("sell_slots",
+           [](const f2m::Graph& g) {
+             f2m_graph_info info{};
+             f2m::check(f2m_graph_get_info(g.handle(), &info));
+             return info.sell_slots;
+           })
+      .def("sweep_bytes", [](const f2m::Graph& g) { return f2m_sweep_algorithmic_bytes(g.handle()); });
+
+  m.def(
+      "build_knn_graph",
+      [](const f2m::Instance& instance, int k, int threads) { return f2m::build_knn_graph(instance, k, threads); },
+      py::arg("instance"), py::arg("k"), py::arg("threads") = 0, py::call_guard<py::gil_scoped_release>());
+  m.def(
+      "graph_from_edges",
+      [](int n, py::array_t<int32_t, py::array::c_style | py::array::forcecast> u,
+         py::array_t<int32_t, py::array::c_style | py::array::forcecast> v,
+         py::array_t<double, py::array::c_style | py::array::forcecast> c) {
+        if (u.size() != v.size() || u.size() != c.size()) throw f2m::ArgumentError("graph_from_edges: length mismatch");
+        f2m_graph* h = nullptr;
+        f2m::check(f2m_graph_from_edges(n, u.size(), u.data(), v.data(), c.data(), &h));
+        return f2m::Graph::adopt(h);
+      },
+      py::arg("n"), py::arg("u"), py::arg("v"), py::arg("cost"));
+  m.def("validate_graph", [](const f2m::Graph& g) {
+    const f2m::GraphReport r = f2m::validate_graph(g);
+    return py::dict(py::arg("min_degree") = r.min_degree, py::arg("max_degree") = r.max_degree,
+                    py::arg("edge_count") = r.edge_count);
+  });
+
+  py::class_<f2m::DualState>(m, "DualState")
+      .def(py::init<>())
+      .def(py::init([](std::vector<double> lam) { return f2m::DualState{std::move(lam)}; }), py::arg("lam"))
+      .def_readwrite("lam", &f2m::DualState::lambda);
+
+  m.def("dual_objective", &f2m::dual_objective, py::arg("graph"), py::arg("state"), py::arg("b") = 2);
+  m.def("adjusted_length", &f2m::adjusted_length, py::arg("graph"), py::arg("state"), py::arg("edge"));
+  m.def("node_update_delta", &f2m::node_update_delta, py::arg("graph"), py::arg("state"), py::arg("node"),
+        py::arg("b") = 2);
+
+  m.def(
+      "solve_duals",
+      [](const f2m::Graph& graph, int b, double eta, double eps, int max_sweeps, const std::string& mode,
+         const std::string& update, const std::string& init, int threads, std::optional<f2m::DualState> initial) {
+        const f2m::EngineConfig config = engine_config(b, eta, eps, max_sweeps, mode, update, init, threads);
+        std::pair<f2m::DualState, f2m::ConvergenceReport> res;
+        {
+          py::gil_scoped_release release;
+          res = f2m::solve_duals(graph, config, initial);
+        }
+        const auto& r = res.second;
+        py::dict rep(py::arg("converged") = r.converged, py::arg("sweeps") = r.sweeps,
+                     py::arg("final_max_abs_delta") = r.final_max_abs_delta, py::arg("dual_value") = r.dual_value,
+                     py::arg("wall_time") = r.wall_time);
+        return py::make_tuple(res.first, rep);
+      },
+      py::arg("graph"), py::arg("b") = 2, py::arg("eta") = 0.5, py::arg("eps") = 1e-9, py::arg("max_sweeps") = 20000,
+      py::arg("mode") = "jacobi", py::arg("update") = "midpoint", py::arg("init") = "local-midpoint",
+      py::arg("threads") = 0, py::arg("initial") = py::none());
+
+  // --- extensions: the sweep-level entry points the reference keeps C++-only (dual.hpp:66-90)
+  m.def(
+      "make_initial_state",
+      [](const f2m::Graph& graph, int b, const std::string& init) {
+        return f2m::make_initial_state(graph, engine_config(b, 0.5, 1e-9, 0, "jacobi", "midpoint", init, 0));
+      },
+      py::arg("graph"), py::arg("b") = 2, py::arg("init") = "local-midpoint");
+  m.def(
+      "jacobi_sweeps",
+      [](const f2m::Graph& graph, f2m::DualState& state, int count, int b, double eta, const std::string& update) {
+        const f2m::EngineConfig c = engine_config(b, eta, 1e-9, 0, "jacobi", update, "local-midpoint", 0);
+        double dv = 0.0;
+        std::vector<double> mx;
+        {
+          py::gil_scoped_release release;
+          mx = f2m::jacobi_sweeps(graph, state, c, count, &dv);
+        }
+        return py::make_tuple(mx, dv);
+      },
+      py::arg("graph"), py::arg("state"), py::arg("count"), py::arg("b") = 2, py::arg("eta") = 0.5,
+      py::arg("update") = "midpoint");
+  m.def(
+      "jacobi_sweep",
+      [](const f2m::Graph& graph, f2m::DualState& state, int b, double eta, const std::string& update) {
+        const f2m::SweepStats s =
+            f2m::jacobi_sweep(graph, state, engine_config(b, eta, 1e-9, 0, "jacobi", update, "local-midpoint", 0));
+        return py::make_tuple(s.max_abs_delta, s.dual_value);
+      },
+      py::arg("graph"), py::arg("state"), py::arg("b") = 2, py::arg("eta") = 0.5, py::arg("update") = "midpoint");
+  m.def(
+      "gauss_seidel_sweep",
+      [](const f2m::Graph& graph, f2m::DualState& state, int b, const std::string& update) {
+        const f2m::SweepStats s = f2m::gauss_seidel_sweep(
+            graph, state, engine_config(b, 0.5, 1e-9, 0, "gauss-seidel", update, "local-midpoint", 0));
+        return py::make_tuple(s.max_abs_delta, s.dual_value);
+      },
+      py::arg("graph"), py::arg("state"), py::arg("b") = 2, py::arg("update") = "midpoint");
+
+  py::class_<f2m::PrimalSolution>(m, "PrimalSolution")
+      .def_readonly("value", &f2m::PrimalSolution::value)
+      .def_readonly("objective", &f2m::PrimalSolution::objective);
+
+  m.def("classify_edges",
+        [](const f2m::Graph& graph, const f2m::DualState& state, double tol) {
+          const f2m::EdgeClassification c = f2m::classify_edges(graph, state, tol);
+          py::array_t<uint8_t> a(static_cast<py::ssize_t>(c.label.size()));
+          for (size_t e = 0; e < c.label.size(); ++e) a.mutable_data()[e] = static_cast<uint8_t>(c.label[e]);
+          return a;
+        },
+        py::arg("graph"), py::arg("state"), py::arg("tol"));
+  m.def("extract_primal", &f2m::extract_primal, py::arg("graph"), py::arg("state"), py::arg("tol"));
+  m.def("solve_zero_component", &f2m::solve_zero_component, py::arg("graph"), py::arg("component_edges"),
+        py::arg("residual"));
+  m.def("verify_solution", [](const f2m::Graph& graph, const f2m::PrimalSolution& solution,
+                              const f2m::DualState& state) {
+    const f2m::VerificationReport r = f2m::verify_solution(graph, solution, state);
+    return py::dict(py::arg("feasible") = r.feasible, py::arg("violated_nodes") = r.violated_nodes,
+                    py::arg("duality_gap") = r.duality_gap, py::arg("value_violations") = r.value_violations);
+  });
+  m.def("write_solution", [](const f2m::Graph& graph, const f2m::PrimalSolution& solution,
+                             const f2m::DualState& state) {
+    std::ostringstream out;
+    f2m::write_solution(graph, solution, f2m::verify_solution(graph, solution, state), out);
+    return out.str();
+  });
+
+  m.def(
+      "brute_force_f2m",
+      [](const f2m::Graph& graph, int max_edges) {
+        const f2m::OracleResult r = f2m::brute_force_f2m(graph, max_edges);
+        return py::dict(py::arg("optimum") = r.optimum, py::arg("value") = r.solution.value,
+                        py::arg("enumerated") = r.enumerated);
+      },
+      py::arg("graph"), py::arg("max_edges") = 20);
+
+  m.def(
+      "full_solve",
+      [](const f2m::Instance& instance, int k, double eta, double eps, int max_sweeps, const std::string& mode,
+         double tol, int max_restarts, std::uint64_t seed, int threads) {
+        f2m::RunConfig config;
+        config.k = k;
+        config.engine = engine_config(2, eta, eps, max_sweeps, mode, "midpoint", "local-midpoint", threads);
+        config.tol = tol;
+        config.max_restarts = max_restarts;
+        config.seed = seed;
+        f2m::SolveOutcome outcome;
+        {
+          py::gil_scoped_release release;
+          outcome = f2m::full_solve(instance, config);
+        }
+        return py::dict(py::arg("objective") = outcome.solution.objective,
+                        py::arg("value") = outcome.solution.value,
+                        py::arg("feasible") = outcome.verification.feasible,
+                        py::arg("gap") = outcome.verification.duality_gap,
+                        py::arg("sweeps") = outcome.convergence.sweeps, py::arg("restarts") = outcome.restarts,
+                        py::arg("duals") = outcome.duals.lambda);
+      },
+      py::arg("instance"), py::arg("k") = 20, py::arg("eta") = 0.5, py::arg("eps") = 1e-9,
+      py::arg("max_sweeps") = 20000, py::arg("mode") = "jacobi", py::arg("tol") = 0.0, py::arg("max_restarts") = 5,
+      py::arg("seed") = 0, py::arg("threads") = 0);
+
+  m.def(
+      "full_solve_graph",
+      [](const f2m::Graph& graph, int k, double eta, double eps, int max_sweeps, const std::string& mode, double tol,
+         int max_restarts, std::uint64_t seed, int threads) {
+        f2m::RunConfig config;
+        config.k = k;
+        config.engine = engine_config(2, eta, eps, max_sweeps, mode, "midpoint", "local-midpoint", threads);
+        config.tol = tol;
+        config.max_restarts = max_restarts;
+        config.seed = seed;
+        f2m::SolveOutcome outcome;
+        {
+          py::gil_scoped_release release;
+          outcome = f2m::full_solve_graph(graph, config);
+        }
+        return py::dict(py::arg("objective") = outcome.solution.objective,
+                        py::arg("value") = outcome.solution.value,
+                        py::arg("feasible") = outcome.verification.feasible,
+                        py::arg("gap") = outcome.verification.duality_gap,
+                        py::arg("sweeps") = outcome.convergence.sweeps, py::arg("restarts") = outcome.restarts,
+                        py::arg("duals") = outcome.duals.lambda);
+      },
+      py::arg("graph"), py::arg("k") = 20, py::arg("eta") = 0.5, py::arg("eps") = 1e-9, py::arg("max_sweeps") = 20000,
+      py::arg("mode") = "jacobi", py::arg("tol") = 0.0, py::arg("max_restarts") = 5, py::arg("seed") = 0,
+      py::arg("threads") = 0);
+
+  // --- C-ABI pipeline entry points with array I/O (benchmark e2e / device-resident paths)
+  m.def(
+      "full_solve_arrays",
+      [](py::array_t<double, py::array::c_style | py::array::forcecast> xy, bool rounded, int k, double eps,
+         int max_sweeps, std::uint64_t seed, int max_restarts, double tol) {
+        const int n = static_cast<int>(xy.size() / 2);
+        const int per = std::max(3, std::min(k, n - 1));
+        f2m_run_config rc = run_config_c(k, 0.5, eps, max_sweeps, "jacobi", tol, max_restarts, seed, 1e-6, 1e-7);
+        std::vector<double> x(static_cast<size_t>(n) * per + 1), lam(static_cast<size_t>(std::max(n, 1)));
+        f2m_solve_outcome o{};
+        f2m_graph* g = nullptr;
+        const double* p = xy.data();
+        int st;
+        {
+          py::gil_scoped_release release;
+          st = f2m_full_solve(n, p, rounded ? 1 : 0, &rc, x.data(), lam.data(), &o, &g);
+        }
+        f2m::check(st);
+        f2m::Graph graph = f2m::Graph::adopt(g);
+        x.resize(static_cast<size_t>(graph.edge_count()));
+        lam.resize(static_cast<size_t>(n));
+        py::dict d = outcome_dict(o);
+        d["value"] = py::array_t<double>(static_cast<py::ssize_t>(x.size()), x.data());
+        d["duals"] = py::array_t<double>(static_cast<py::ssize_t>(lam.size()), lam.data());
+        d["graph"] = graph;
+        return d;
+      },
+      py::arg("xy"), py::arg("rounded") = false, py::arg("k") = 10, py::arg("eps") = 1e-9,
+      py::arg("max_sweeps") = 20000, py::arg("seed") = 0, py::arg("max_restarts") = 5, py::arg("tol") = 0.0);
+  m.def(
+      "full_solve_device",
+      [](int n, std::uintptr_t d_xy, bool rounded, int k, double eps, int max_sweeps, std::uintptr_t d_x,
+         std::int64_t x_capacity, std::uintptr_t d_lambda, std::uint64_t seed, int max_restarts) {
+        f2m_run_config rc = run_config_c(k, 0.5, eps, max_sweeps, "jacobi", 0.0, max_restarts, seed, 1e-6, 1e-7);
+        f2m_solve_outcome o{};
+        int st;
+        {
+          py::gil_scoped_release release;
+          st = f2m_full_solve_device(n, reinterpret_cast<const double*>(d_xy), rounded ? 1 : 0, &rc,
+                                     reinterpret_cast<double*>(d_x), x_capacity,
+                                     reinterpret_cast<double*>(d_lambda), &o, nullptr);
+        }
+        f2m::check(st);
+        return outcome_dict(o);
+      },
+      py::arg("n"), py::arg("d_xy"), py::arg("rounded"), py::arg("k"), py::arg("eps"), py::arg("max_sweeps"),
+      py::arg("d_x"), py::arg("x_capacity"), py::arg("d_lambda"), py::arg("seed") = 0, py::arg("max_restarts") = 5);
+
+  m.def("write_lp", [](const f2m::Graph& graph) {
+    std::ostringstream out;
+    f2m::write_lp(graph, out);
+    return out.str();
+  });
+
+  // --- observability
+  m.def("device_info", []() {
+    f2m_device_info d{};
+    f2m::check(f2m_get_device_info(&d));
+    return py::dict(py::arg("device") = d.device, py::arg("sm_count") = d.sm_count,
+                    py::arg("sweep_ctas") = d.sweep_ctas, py::arg("sweep_threads") = d.sweep_threads,
+                    py::arg("cc") = std::to_string(d.cc_major) + "." + std::to_string(d.cc_minor),
+                    py::arg("name") = std::string(d.name));
+  });
+  m.def("set_device", [](int dev) { f2m::check(f2m_set_device(dev)); }, py::arg("device"));
+  m.def("kernel_launch_count", []() { return f2m_kernel_launch_count(); });
+  m.def("last_sweep_kernel", []() {
+    double ms = 0.0;
+    int sweeps = 0;
+    f2m_last_sweep_kernel_ms(&ms, &sweeps);
+    return py::make_tuple(ms, sweeps);
+  });
+}

@@ -1,0 +1,235 @@
+"""GPU parity: the GDP engine (dual.cpp) — init, Jacobi sweeps, convergence, dual objective.
+
+Bar: bit-exact fp64 (lambda arrays compared by SHA-256 / array_equal, scalars with ==) against
+golden fixtures from the unmodified reference, plus the reference's own KATs (test_dual.cpp).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def _graph(f2m, name):
+    meta, arrays = golden(name)
+    a = meta["args"]
+    i = a.index("--synthetic")
+    inst = f2m.generate_instance(int(a[i + 1]), int(a[i + 2]), float(a[i + 3]))
+    if "--rounded" in a:
+        inst.mode = f2m.DistanceMode.EUC2D_ROUNDED
+    g = f2m.build_knn_graph(inst, int(a[a.index("--k") + 1]))
+    return g, meta, arrays
+
+
+@pytest.mark.parametrize("name", ["u1k_s1", "c6_u10k_s4242", "u10k_s1", "u500_s21_b100_k6",
+                                  "u2k_s17_b300_k6_zero", "u10k_s1_k20_rounded"])
+def test_initial_state_bit_exact(f2m, name):
+    g, meta, _ = _graph(f2m, name)
+    st = f2m.make_initial_state(g, init=meta["init"])
+    assert sha(np.array(st.lam)) == meta["sha256"]["lam0"]
+
+
+@pytest.mark.parametrize("name", ["u1k_s1", "c6_u10k_s4242", "u500_s21_b100_k6", "u2k_s17_b300_k6_zero",
+                                  "u1k_s7_eta03", "u10k_s1_k20_rounded", "u10k_s1"])
+def test_jacobi_sweeps_bit_exact(f2m, name):
+    """lambda and max|delta| after every sweep, and g(lambda) after the last (parity ladder L2)."""
+    g, meta, _ = _graph(f2m, name)
+    st = f2m.make_initial_state(g, init=meta["init"])
+    count = meta["sweeps_dumped"]
+    mx, dual = f2m.jacobi_sweeps(g, st, count, eta=meta["eta"])
+    stats = np.array(meta["sweep_stats"])
+    assert np.array_equal(np.array(mx), stats[:, 0])
+    assert dual == stats[-1, 1]
+    assert sha(np.array(st.lam)) == meta["sha256"]["lamN"]
+
+
+def test_c6_golden_dual_value(f2m):
+    # acceptance criterion 6: 100 sweeps on uniform 10k seed 4242 -> dual 68422.67083340639
+    g, meta, _ = _graph(f2m, "c6_u10k_s4242")
+    st, rep = f2m.solve_duals(g, eps=1e-300, max_sweeps=100)
+    assert rep["sweeps"] == 100 and not rep["converged"]
+    assert rep["dual_value"] == 68422.67083340639
+    assert sha(np.array(st.lam)) == meta["sha256"]["lamN"]
+
+
+def test_per_sweep_dual_values(f2m):
+    # jacobi_sweep reports g(lambda) every sweep (dual.cpp:165)
+    g, meta, arrays = _graph(f2m, "u1k_s1")
+    st = f2m.make_initial_state(g)
+    for mx_ref, dv_ref in meta["sweep_stats"][:8]:
+        mx, dv = f2m.jacobi_sweep(g, st)
+        assert mx == mx_ref and dv == dv_ref
+
+
+@pytest.mark.parametrize("name", ["u1k_s1", "u1k_s2", "u1k_s3", "u1k_s4", "u1k_s5", "u10k_s1",
+                                  "u500_s21_b100_k6", "u2k_s17_b300_k6_zero"])
+def test_solve_duals_converges_like_reference(f2m, name):
+    """Sweep count, final lambda, final max|delta| and dual value (parity ladder L3)."""
+    g, meta, _ = _graph(f2m, name)
+    st, rep = f2m.solve_duals(g, eps=meta["eps"], max_sweeps=meta["max_sweeps"], init=meta["init"])
+    assert rep["sweeps"] == meta["sweeps"]
+    assert rep["converged"] == bool(meta["converged"])
+    assert rep["final_max_abs_delta"] == meta["final_max_abs_delta"]
+    assert rep["dual_value"] == meta["dual_value"]
+    assert sha(np.array(st.lam)) == meta["sha256"]["lam_final"]
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+@pytest.mark.parametrize("update", ["midpoint", "paper-difference"])
+def test_sweeps_vs_oracle_b_and_rule(f2m, orc, b, update):
+    xy = orc.generate_instance(1500, 77 + b, 500.0)
+    og = orc.build_knn_graph(xy, 8)
+    g = f2m.build_knn_graph(f2m.Instance.from_points(xy), 8)
+    lam0 = orc.initial_state(og, b=b)
+    st = f2m.make_initial_state(g, b=b)
+    assert np.array_equal(np.array(st.lam), lam0)
+    mx, dv = f2m.jacobi_sweeps(g, st, 12, b=b, update=update, eta=0.7)
+    for s in range(12):
+        omx, odv = orc.jacobi_sweep(og, lam0, b=b, update=update, eta=0.7)
+        assert mx[s] == omx
+    assert dv == odv
+    assert np.array_equal(np.array(st.lam), lam0)
+
+
+def test_gauss_seidel_vs_oracle(f2m, orc):
+    xy = orc.generate_instance(300, 5, 100.0)
+    og = orc.build_knn_graph(xy, 6)
+    g = f2m.build_knn_graph(f2m.Instance.from_points(xy), 6)
+    lam = np.zeros(300)
+    st = f2m.DualState([0.0] * 300)
+    for _ in range(5):
+        omx, odv = orc.gauss_seidel_sweep(og, lam)
+        mx, dv = f2m.gauss_seidel_sweep(g, st)
+        assert mx == omx and dv == odv
+    assert np.array_equal(np.array(st.lam), lam)
+    ost, orep = orc.solve_duals(og, mode="gauss-seidel")
+    st2, rep = f2m.solve_duals(g, mode="gauss-seidel")
+    assert rep["sweeps"] == orep["sweeps"] and rep["dual_value"] == orep["dual_value"]
+    assert np.array_equal(np.array(st2.lam), ost)
+
+
+def test_dual_objective_chunk_order(f2m, orc):
+    # > one node chunk (2048) and > one edge chunk (8192): the reference's summation order
+    xy = orc.generate_instance(5000, 3, 1000.0)
+    og = orc.build_knn_graph(xy, 10)
+    g = f2m.build_knn_graph(f2m.Instance.from_points(xy), 10)
+    rng = np.random.default_rng(0)
+    for trial in range(3):
+        lam = rng.normal(10.0, 5.0, 5000)
+        for b in (1, 2, 3):
+            assert f2m.dual_objective(g, f2m.DualState(lam.tolist()), b) == orc.dual_objective(og, lam, b)
+
+
+def _star(f2m, costs):
+    k = len(costs)
+    return f2m.graph_from_edges(k + 1, [0] * k, list(range(1, k + 1)), list(map(float, costs)))
+
+
+def test_midpoint_kats(f2m):
+    # test_dual.cpp:60-76
+    g1 = _star(f2m, [8, 9, 13, 15])
+    assert f2m.node_update_delta(g1, f2m.DualState([10.0, 0, 0, 0, 0]), 0, 2) == pytest.approx(1.0, abs=1e-15)
+    g2 = _star(f2m, [7, 9, 11, 14])
+    assert f2m.node_update_delta(g2, f2m.DualState([10.0, 0, 0, 0, 0]), 0, 2) == pytest.approx(0.0, abs=1e-15)
+    g3 = _star(f2m, [1, 2])
+    with pytest.raises(RuntimeError):  # DegreeError
+        f2m.node_update_delta(g3, f2m.DualState([0.0, 0, 0]), 0, 2)
+    with pytest.raises(IndexError):
+        f2m.node_update_delta(g3, f2m.DualState([0.0, 0, 0]), 5, 2)
+
+
+def test_adjusted_length(f2m):
+    # test_dual.cpp:34-42
+    g = f2m.graph_from_edges(2, [0], [1], [10.0])
+    assert f2m.adjusted_length(g, f2m.DualState([0.0, 0.0]), 0) == 10.0
+    assert f2m.adjusted_length(g, f2m.DualState([3.0, 4.0]), 0) == 3.0
+    with pytest.raises(IndexError):
+        f2m.adjusted_length(g, f2m.DualState([3.0, 4.0]), 1)
+
+
+def _unit_square(f2m):
+    return f2m.Instance.from_points(np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float))
+
+
+def test_unit_square_dual_and_fixed_point(f2m):
+    # test_dual.cpp:108-115, 133-142
+    g = f2m.build_knn_graph(_unit_square(f2m), 3)
+    assert f2m.dual_objective(g, f2m.DualState([0.0] * 4)) == 0.0
+    assert f2m.dual_objective(g, f2m.DualState([0.5] * 4)) == pytest.approx(4.0, abs=1e-14)
+    a = (1.0 + math.sqrt(2.0)) / 4.0
+    st = f2m.DualState([a] * 4)
+    mx, dv = f2m.jacobi_sweep(g, st)
+    assert mx <= 1e-15
+    assert dv == pytest.approx(4.0)
+    for l in st.lam:
+        assert l == pytest.approx(a, rel=1e-15)
+
+
+def test_config_validation(f2m):
+    # test_dual.cpp:117-131 (+ the b <= 8 bound the reference misses)
+    g = f2m.build_knn_graph(_unit_square(f2m), 3)
+    for kw in (dict(eta=0.0), dict(eta=1.5), dict(eps=0.0), dict(b=0), dict(b=9), dict(max_sweeps=-1)):
+        with pytest.raises(ValueError):
+            f2m.solve_duals(g, **kw)
+
+
+@pytest.mark.parametrize("mode", ["jacobi", "gauss-seidel"])
+def test_unit_square_optimum(f2m, mode):
+    # test_dual.cpp:205-215
+    g = f2m.build_knn_graph(_unit_square(f2m), 3)
+    st, rep = f2m.solve_duals(g, mode=mode)
+    assert rep["converged"]
+    assert rep["dual_value"] == pytest.approx(4.0, rel=1e-6)
+    assert rep["final_max_abs_delta"] <= 1e-9 * g.mean_cost()
+
+
+def test_zero_budget_and_initial_state(f2m):
+    # test_dual.cpp:217-238
+    g = f2m.build_knn_graph(_unit_square(f2m), 3)
+    st, rep = f2m.solve_duals(g, max_sweeps=0, init="zero")
+    assert not rep["converged"] and rep["sweeps"] == 0
+    assert st.lam == [0.0] * 4 and rep["dual_value"] == 0.0
+    assert math.isinf(rep["final_max_abs_delta"])
+    a = (1.0 + math.sqrt(2.0)) / 4.0
+    st, rep = f2m.solve_duals(g, initial=f2m.DualState([a] * 4))
+    assert rep["converged"] and rep["sweeps"] == 1
+    with pytest.raises(ValueError):
+        f2m.solve_duals(g, initial=f2m.DualState([0.0]))
+
+
+def test_degree_error(f2m):
+    g = _star(f2m, [1, 2, 3])  # leaves have degree 1
+    with pytest.raises(RuntimeError, match="degree"):
+        f2m.solve_duals(g)
+
+
+def test_gauss_seidel_monotone(f2m):
+    # test_dual.cpp:163-188 / acceptance criterion 3
+    for seed in range(6):
+        inst = f2m.generate_instance(24 + seed, seed, 100.0)
+        g = f2m.build_knn_graph(inst, 6)
+        st = f2m.DualState([0.0] * g.n)
+        prev = f2m.dual_objective(g, st)
+        for _ in range(10):
+            _, dv = f2m.gauss_seidel_sweep(g, st)
+            assert dv >= prev - 1e-9 * g.mean_cost()
+            prev = dv
+
+
+def test_local_update_contract(f2m):
+    # test_dual.cpp:90-106 / acceptance criterion 4
+    rng = np.random.default_rng(4)
+    for seed in range(5):
+        inst = f2m.generate_instance(25, seed, 10.0)
+        g = f2m.build_knn_graph(inst, 5)
+        lam = ((rng.random(25) - 0.5) * 10.0).tolist()
+        edges = g.edges()
+        for v in range(0, 25, 3):
+            t = list(lam)
+            t[v] += f2m.node_update_delta(g, f2m.DualState(t), v, 2)
+            vals = sorted(c - t[a] - t[b] for a, b, c in edges if a == v or b == v)
+            assert abs(vals[1] + vals[2]) <= 1e-12
+            assert vals[1] <= 1e-12 and vals[2] >= -1e-12
