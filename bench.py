@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: F2M time-to-solve on random-uniform 100,000 cities (BASELINE.json configs[2]).
+
+One step = one certified full solve — k-NN candidate graph (k=10) -> local-midpoint init ->
+Jacobi GDP sweeps to max|delta| <= 1e-9*mean_cost -> extraction -> duality certificate — of a
+synthetic uniform instance (generate_instance(100000, seed=1, box=1000), the reference's own
+generator), i.e. the reference's full_solve (solve.cpp:101-106).
+
+  value      device time per solve with the points already resident in HBM and x / lambda
+             left in HBM (CUDA events on the solve's stream), via f2m_full_solve_device.
+  e2e        the same solve through the public C ABI with host buffers (f2m_full_solve via the
+             pybind module): pinned host points -> device, x and lambda -> host, wall clock.
+  roofline   the dominant kernel, the persistent GDP sweep kernel: algorithmic bytes per launch
+             (4(n+1) + 2m*12 + 16n per sweep, times the sweeps of the launch)
+             over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the unmodified reference (oracle/_ref, compiled from /root/reference) on this
+             host: build_knn_graph + 100 Jacobi sweeps timed, extraction + verification timed on
+             the converged multipliers, full solve projected to the reference's own sweep count.
+
+--impl reference runs only that reference leg (rank 0), printing the same JSON line shape.
+Multi-GPU (torchrun, N>1): every rank solves its own replica (weak scaling, no data-path
+collective); node-sharded single-instance solving is future work.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_CITIES = 100_000
+SEED = 1
+K = 10
+EPS = 1e-9
+MAX_SWEEPS = 200_000
+REF_SAMPLE_SWEEPS = 100
+METRIC = "F2M time-to-solve (s), random-uniform 100k cities, k=10"
+WORKLOAD = ("random-uniform 100,000 cities (generate_instance seed 1, box 1000, EUC2D exact), "
+            "k=10 candidate lists, Jacobi GDP eta=0.5 eps=1e-9, certified full solve (BASELINE configs[2])")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _traffic():
+    """dram bytes per sweep-kernel launch from the committed ncu capture summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            s = json.load(f)
+        return s.get("gdp_sweep", {}).get("dram_bytes_per_launch"), s.get("gdp_sweep", {}).get("sweeps_per_launch")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def reference_sample(sweeps_total: int, lam_converged=None):
+    """Bounded sample of the unmodified reference on this host, 1 thread (its ThreadPool races
+    for >1 thread). Returns (projected seconds, detail dict)."""
+    ref_path = os.path.join(ROOT, "oracle", "_ref")
+    if ref_path not in sys.path:
+        sys.path.insert(0, ref_path)
+    import f2m as ref  # the reference's own pybind module, compiled from /root/reference sources
+
+    inst = ref.generate_instance(N_CITIES, SEED, 1000.0)
+    t0 = time.perf_counter()
+    g = ref.build_knn_graph(inst, K, threads=1)
+    t_knn = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st0, rep0 = ref.solve_duals(g, eps=EPS, max_sweeps=0, threads=1)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st, rep = ref.solve_duals(g, eps=1e-300, max_sweeps=REF_SAMPLE_SWEEPS, threads=1)
+    t_sample = time.perf_counter() - t0
+    per_sweep = (t_sample - t_init) / REF_SAMPLE_SWEEPS
+    t_extract = None
+    if lam_converged is not None:
+        st.lam = list(lam_converged)
+        t0 = time.perf_counter()
+        sol = ref.extract_primal(g, st, max(1e-7, 10 * EPS) * g.mean_cost())
+        ref.verify_solution(g, sol, st)
+        t_extract = time.perf_counter() - t0
+    projected = t_knn + t_init + per_sweep * sweeps_total + (t_extract or 0.0)
+    detail = {"t_knn": t_knn, "t_init": t_init, "per_sweep_s": per_sweep, "sample_sweeps": REF_SAMPLE_SWEEPS,
+              "t_extract_verify": t_extract, "sweeps_projected": sweeps_total, "m": g.m}
+    return projected, detail
+
+
+def _golden_sweeps():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "u100k_s1.json")) as f:
+            return int(json.load(f)["sweeps"]), "tests/golden/u100k_s1.json (reference run)"
+    except Exception:
+        return 6359, "SURVEY.md §6 (reference run, 100k seed 1)"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    sweeps, src = _golden_sweeps()
+    vals = []
+    detail = None
+    for i in range(args.warmup + args.steps):
+        v, detail = reference_sample(sweeps)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    sample = (f"per step: reference build_knn_graph(100k, k=10) + init + {REF_SAMPLE_SWEEPS} Jacobi sweeps "
+              f"timed on 1 host core; full solve projected to {sweeps} sweeps ({src})")
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": "1 host thread"},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "reference", "sample": sample,
+                         "detail": detail},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_2011_08170_b200 as f2m
+    f2m.set_device(local)
+    dev = torch.device("cuda", local)
+
+    inst = f2m.generate_instance(N_CITIES, SEED, 1000.0)
+    xy_host = inst.points_array()
+    xy_pinned = torch.from_numpy(xy_host).pin_memory()
+    d_xy = xy_pinned.to(dev)
+    cap = N_CITIES * K
+    d_x = torch.empty(cap, dtype=torch.float64, device=dev)
+    d_lam = torch.empty(N_CITIES, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MB > 126 MB L2
+
+    def solve_device():
+        return f2m.full_solve_device(N_CITIES, d_xy.data_ptr(), False, K, EPS, MAX_SWEEPS, d_x.data_ptr(), cap,
+                                     d_lam.data_ptr())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    # ---- value: inputs resident in HBM, outputs left in HBM
+    for _ in range(args.warmup):
+        flush.zero_()
+        solve_device()
+    times, sweep_ms, sweeps = [], [], []
+    barrier()
+    launches0 = f2m.kernel_launch_count()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()                     # L2 flushed between timed solves
+            torch.cuda.synchronize()
+            r = solve_device()
+            times.append(r["t_total"])        # CUDA events on the solve's own stream
+            ms, sw = f2m.last_sweep_kernel()
+            sweep_ms.append(ms)
+            sweeps.append(sw)
+    barrier()
+    wall = time.perf_counter() - wall0
+    launches = (f2m.kernel_launch_count() - launches0) / max(args.steps, 1)
+    t_step = statistics.mean(times)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+
+    # ---- e2e: host buffers through the public C ABI (H2D points, D2H x and lambda)
+    for _ in range(max(1, args.warmup // 2)):
+        f2m.full_solve_arrays(xy_pinned.numpy(), k=K, eps=EPS, max_sweeps=MAX_SWEEPS)
+    e2e_times = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr = f2m.full_solve_arrays(xy_pinned.numpy(), k=K, eps=EPS, max_sweeps=MAX_SWEEPS)
+        e2e_times.append(time.perf_counter() - t0)
+    barrier()
+    e2e = statistics.mean(e2e_times)
+    m = int(rr["graph"].m)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+    assert rr["sweeps"] == r["sweeps"] and rr["objective"] == r["objective"]
+
+    # ---- roofline of the dominant kernel (persistent GDP sweep)
+    bytes_per_sweep = rr["graph"].sweep_bytes()
+    sw = statistics.median(sweeps)
+    kern_ms = statistics.median(sweep_ms)
+    achieved = bytes_per_sweep * sw / (kern_ms * 1e-3) / 1e9
+    peak, peak_src = _peaks()
+    dram, dram_sweeps = _traffic()
+    traffic = None
+    if dram is not None and dram_sweeps:
+        traffic = dram / dram_sweeps * sw  # per launch of this run's sweep count
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_gdp_sweep<2> (persistent, 148 CTAs x 1024 threads)",
+                "algorithmic_bytes_per_sweep": bytes_per_sweep, "sweeps_per_launch": sw,
+                "kernel_ms": kern_ms, "us_per_sweep": 1e3 * kern_ms / sw, "peak_source": peak_src,
+                "share_of_step": (kern_ms * 1e-3) / t_step}
+
+    line = {
+        "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generator, seed 1)",
+        "config": {"workload": WORKLOAD, "n": N_CITIES, "m": m, "k": K, "eps": EPS,
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                   "l2": "512 MB write between timed steps (working set ~30 MB < 126 MB L2)"},
+        "gdp_iterations_per_s": sw / (kern_ms * 1e-3),
+        "sweeps": int(sw), "objective": r["objective"], "gap": r["gap"], "restarts": r["restarts"],
+        "stage_s": {"knn": r["t_knn"], "duals": r["t_duals"], "extract_verify": r["t_extract"]},
+        "roofline": roofline,
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 16 * N_CITIES,
+                "d2h_bytes_per_step": 8 * m + 8 * N_CITIES},
+        "gpu_launches": int(round(launches)),
+        "clocks": clocks.summary(),
+        "wall_s_timed_region": wall,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        sweeps_total = int(sw)
+        lam = d_lam.cpu().numpy()
+        v, detail = reference_sample(sweeps_total, lam)
+        line["cpu_baseline"] = {
+            "value": v, "unit": "s", "cores": 1, "kind": "reference",
+            "sample": (f"unmodified reference (oracle/_ref): build_knn_graph + init + {REF_SAMPLE_SWEEPS} Jacobi "
+                       f"sweeps + extract/verify on the converged lambda, 1 thread; projected to "
+                       f"{sweeps_total} sweeps"),
+            "detail": detail}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -241,3 +241,24 @@ def test_smoke_surface_like_reference(f2m):
     sol = f2m.extract_primal(g, st, tol=1e-7 * g.mean_cost())
     v = f2m.verify_solution(g, sol, st)
     assert v["feasible"] and abs(v["duality_gap"]) <= 1e-9
+
+
+def test_brute_force_oracle_kats(f2m):
+    # test_oracle.cpp:60-97 (host enumerator = independent ground truth)
+    tri = f2m.Instance.from_points(np.array([[0, 0], [3, 0], [0, 4]], float))
+    g = f2m.graph_from_edges(3, [0, 0, 1], [1, 2, 2], [tri.distance(0, 1), tri.distance(0, 2), tri.distance(1, 2)])
+    r = f2m.brute_force_f2m(g)
+    assert r["optimum"] == pytest.approx(12.0, rel=1e-15) and r["value"] == [1.0, 1.0, 1.0]
+    sq = f2m.build_knn_graph(_sq(f2m), 3)
+    r = f2m.brute_force_f2m(sq)
+    assert r["optimum"] == pytest.approx(4.0, rel=1e-15) and r["enumerated"] >= 1
+    k5u, k5v = zip(*[(u, v) for u in range(5) for v in range(u + 1, 5)])
+    assert f2m.brute_force_f2m(f2m.graph_from_edges(5, k5u, k5v, [1.0] * 10))["optimum"] == pytest.approx(5.0)
+    g7 = f2m.build_knn_graph(f2m.generate_instance(7, 1, 10.0), 6)
+    with pytest.raises(f2m.TooLarge):
+        f2m.brute_force_f2m(g7)
+    assert f2m.brute_force_f2m(g7, 21)["optimum"] > 0.0
+    with pytest.raises(f2m.Infeasible):
+        f2m.brute_force_f2m(f2m.graph_from_edges(2, [0], [1], [1.0]))
+    with pytest.raises(f2m.Infeasible):
+        f2m.brute_force_f2m(f2m.graph_from_edges(4, [0, 1, 2], [1, 2, 3], [1.0, 1.0, 1.0]))

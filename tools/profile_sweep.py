@@ -1,0 +1,15 @@
+"""Run exactly one persistent GDP sweep-kernel launch (for ncu): python tools/profile_sweep.py N SWEEPS."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2011_08170_b200 as f2m  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
+sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+g = f2m.build_knn_graph(f2m.generate_instance(n, 1), 10)
+st = f2m.make_initial_state(g)
+mx, dv = f2m.jacobi_sweeps(g, st, sweeps)
+ms, sw = f2m.last_sweep_kernel()
+print(f"n={n} m={g.m} sweeps={sw} kernel_ms={ms:.3f} us/sweep={1e3 * ms / sw:.3f} "
+      f"bytes/sweep={g.sweep_bytes():.0f} GB/s={g.sweep_bytes() * sw / (ms * 1e-3) / 1e9:.1f}")
