@@ -101,6 +101,11 @@ typedef struct {
   int min_degree;
   int max_degree;
   int64_t sell_slots; /* padded SELL-32 slot count (>= 2m) */
+  int sweep_ctas;      /* CTAs of the persistent sweep kernel (<= SM count) */
+  int sweep_variant;   /* 1 = grid-barrier kernel, 2 = neighbour-synchronised (smem-staged), 3 = 2 + smem-resident slots */
+  int max_local;       /* max over CTAs of own + halo nodes (v2 local index space) */
+  int64_t max_cta_slots; /* max over CTAs of padded slots */
+  int64_t smem_bytes;  /* dynamic shared memory of the v2 kernel */
 } f2m_graph_info;
 int f2m_graph_get_info(const f2m_graph* g, f2m_graph_info* out);
 

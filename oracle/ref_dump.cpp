@@ -47,7 +47,7 @@ int main(int argc, char** argv) {
   Instance inst;
   int k = 10, sweeps = 0, max_sweeps = 20000;
   double eps = 1e-9, eta = 0.5;
-  bool rounded = false, solve = true;
+  bool rounded = false, solve = true, full_only = false;
   std::uint64_t jitter_seed = 0;
   std::string init = "local-midpoint";
   for (int i = 2; i < argc; ++i) {
@@ -80,6 +80,8 @@ int main(int argc, char** argv) {
       init = argv[++i];
     } else if (a == "--no-solve") {
       solve = false;
+    } else if (a == "--full-only") {
+      full_only = true;
     } else if (a == "--seed") {
       jitter_seed = std::strtoull(argv[++i], nullptr, 10);
     } else {
@@ -138,7 +140,23 @@ int main(int argc, char** argv) {
                "\"max_sweeps\": %d, \"t_knn\": %.6f",
                n, g.edge_count(), k, rounded ? 1 : 0, g.mean_cost(), sweeps, eps, eta, init.c_str(),
                max_sweeps, t_knn);
-  if (solve) {
+  if (solve && full_only) {
+    RunConfig rc;
+    rc.k = k;
+    rc.engine = cfg;
+    rc.seed = jitter_seed;
+    t0 = now();
+    SolveOutcome out = full_solve_graph(g, rc);
+    const double t_full = now() - t0;
+    dump(dir, "x_full.f64", out.solution.value);
+    dump(dir, "lam_full.f64", out.duals.lambda);
+    std::fprintf(meta, ", \"full_ok\": 1, \"full_objective\": %.17g, \"full_gap\": %.17g, "
+                 "\"full_restarts\": %d, \"full_sweeps\": %d, \"full_feasible\": %d, \"t_full\": %.6f, "
+                 "\"sweeps\": %d, \"dual_value\": %.17g, \"final_max_abs_delta\": %.17g, \"converged\": %d",
+                 out.solution.objective, out.verification.duality_gap, out.restarts, out.convergence.sweeps,
+                 out.verification.feasible ? 1 : 0, t_full, out.convergence.sweeps, out.convergence.dual_value,
+                 out.convergence.final_max_abs_delta, out.convergence.converged ? 1 : 0);
+  } else if (solve) {
     t0 = now();
     auto [lam, rep] = solve_duals(g, cfg);
     const double t_solve = now() - t0;

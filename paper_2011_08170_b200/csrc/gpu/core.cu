@@ -37,6 +37,8 @@ Topology::~Topology() {
     cudaSetDevice(dev);
     eu.release(); ev.release(); perm.release(); iperm.release(); deg.release();
     sptr.release(); swidth.release(); scol.release(); seid.release(); cta_lo.release();
+    halo_off.release(); halo.release(); slidx.release(); nbr_off.release(); nbr.release();
+    cta_int_hi.release();
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
@@ -252,6 +254,160 @@ __global__ void k_incidence_keys(int64_t m, const int32_t* __restrict__ eu,
   if (ev[e] != eu[e]) ids[off[ev[e]] + atomicAdd(&cur[ev[e]], 1)] = (int32_t)e;
 }
 
+
+// ---- permutation application: position i takes the node previously at old_of_new[i]
+__global__ void k_window_apply(int n, const int32_t* __restrict__ old_of_new, const int32_t* __restrict__ deg_old,
+                               const int32_t* __restrict__ iperm_old, int32_t* __restrict__ deg_new,
+                               int32_t* __restrict__ iperm_new, int32_t* __restrict__ perm_new) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int o = old_of_new[i];
+  deg_new[i] = deg_old[o];
+  const int orig = iperm_old[o];
+  iperm_new[i] = orig;
+  perm_new[orig] = i;
+}
+
+
+// ---- CTA partition and CTA-local node order (sweep kernel v3)
+__global__ void k_slice_weight(int n, int64_t nslices, const int32_t* __restrict__ deg, int64_t* __restrict__ w) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  int64_t acc = 0;
+  for (int l = 0; l < 32; ++l) {
+    const int64_t p = s * 32 + l;
+    if (p < n) acc += deg[p];
+  }
+  w[s] = acc;
+}
+
+__global__ void k_boundary(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                           const int32_t* __restrict__ perm, const int32_t* __restrict__ cos,
+                           uint8_t* __restrict__ bnd) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const int pu = perm[eu[e]], pv = perm[ev[e]];
+  if (cos[pu >> 5] != cos[pv >> 5]) {
+    bnd[pu] = 1;
+    bnd[pv] = 1;
+  }
+}
+
+__global__ void k_local_keys(int n, const int32_t* __restrict__ deg, const uint8_t* __restrict__ bnd,
+                             const int32_t* __restrict__ cos, uint64_t* __restrict__ key,
+                             int32_t* __restrict__ val, int32_t* __restrict__ nint) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int c = cos[p >> 5];
+  // CTA (keeps the partition), interior before boundary, then degree descending
+  key[p] = ((uint64_t)(uint32_t)c << 40) | ((uint64_t)bnd[p] << 32) | (uint32_t)(0x7fffffff - deg[p]);
+  val[p] = p;
+  if (!bnd[p]) atomicAdd(&nint[c], 1);
+}
+
+__global__ void k_int_hi(int ctas, const int32_t* __restrict__ lo, const int32_t* __restrict__ nint,
+                         int32_t* __restrict__ int_hi) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ctas) int_hi[c] = lo[c] + nint[c] / 32;  // whole slices of interior nodes
+}
+
+// ---- v2 local index space
+__global__ void k_cta_of_slice(int ctas, const int32_t* __restrict__ lo, int32_t* __restrict__ cos) {
+  const int c = blockIdx.x;
+  for (int s = lo[c] + threadIdx.x; s < lo[c + 1]; s += blockDim.x) cos[s] = c;
+}
+
+__device__ __forceinline__ void own_range(int c, int n, const int32_t* __restrict__ lo, int& p0, int& p1) {
+  p0 = lo[c] * 32;
+  p1 = min(lo[c + 1] * 32, n);
+  if (p1 < p0) p1 = p0;
+}
+
+// one warp per slice: halo key (cta << 32 | q) for every neighbour q outside the owner's range
+__global__ void k_halo_keys(int n, int64_t nslices, const int64_t* __restrict__ sptr,
+                            const int32_t* __restrict__ scol, const int32_t* __restrict__ seid,
+                            const int32_t* __restrict__ cos, const int32_t* __restrict__ lo,
+                            uint64_t* __restrict__ keys) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  const int c = cos[s];
+  int p0, p1;
+  own_range(c, n, lo, p0, p1);
+  for (int64_t t = sptr[s] + lane; t < sptr[s + 1]; t += 32) {
+    const int q = scol[t];
+    const bool halo = seid[t] >= 0 && (q < p0 || q >= p1);
+    keys[t] = halo ? (((uint64_t)(uint32_t)c << 32) | (uint32_t)q) : ~0ULL;
+  }
+}
+
+__global__ void k_halo_split(int64_t h, const uint64_t* __restrict__ keys, int32_t* __restrict__ halo,
+                             int32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= h) return;
+  halo[i] = (int32_t)(keys[i] & 0xffffffffu);
+  atomicAdd(&cnt[keys[i] >> 32], 1);
+}
+
+__global__ void k_local_sizes(int ctas, int n, const int32_t* __restrict__ lo, const int32_t* __restrict__ hoff,
+                              const int64_t* __restrict__ sptr, int* __restrict__ max_local,
+                              unsigned long long* __restrict__ max_slots) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ctas) return;
+  int p0, p1;
+  own_range(c, n, lo, p0, p1);
+  atomicMax(max_local, (p1 - p0) + (hoff[c + 1] - hoff[c]));
+  atomicMax(max_slots, (unsigned long long)(sptr[lo[c + 1]] - sptr[lo[c]]));
+}
+
+__global__ void k_slot_lidx(int n, int64_t nslices, const int64_t* __restrict__ sptr,
+                            const int32_t* __restrict__ scol, const int32_t* __restrict__ seid,
+                            const int32_t* __restrict__ cos, const int32_t* __restrict__ lo,
+                            const int32_t* __restrict__ hoff, const int32_t* __restrict__ halo,
+                            uint16_t* __restrict__ slidx) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  const int c = cos[s];
+  int p0, p1;
+  own_range(c, n, lo, p0, p1);
+  const int own = p1 - p0;
+  const int h0 = hoff[c], h1 = hoff[c + 1];
+  const int p = (int)(s * 32 + lane);
+  for (int64_t t = sptr[s] + lane; t < sptr[s + 1]; t += 32) {
+    int li;
+    if (seid[t] < 0) {
+      li = min(max(p - p0, 0), max(own - 1, 0));  // padding: own slot, cost +inf
+    } else {
+      const int q = scol[t];
+      if (q >= p0 && q < p1) {
+        li = q - p0;
+      } else {
+        int a = h0, b = h1;
+        while (a < b) { const int mid = (a + b) >> 1; if (halo[mid] < q) a = mid + 1; else b = mid; }
+        li = own + (a - h0);
+      }
+    }
+    slidx[t] = (uint16_t)li;
+  }
+}
+
+// CTA adjacency: owner of every halo node (halo sorted by (cta, q); owners are monotone in q)
+__global__ void k_nbr_keys(int ctas, const int32_t* __restrict__ hoff, const int32_t* __restrict__ halo,
+                           const int32_t* __restrict__ cos, uint64_t* __restrict__ keys) {
+  const int c = blockIdx.x;
+  for (int i = hoff[c] + threadIdx.x; i < hoff[c + 1]; i += blockDim.x)
+    keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)cos[halo[i] >> 5];
+}
+
+__global__ void k_nbr_split(int64_t k, const uint64_t* __restrict__ keys, int32_t* __restrict__ nbr,
+                            int32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  nbr[i] = (int32_t)(keys[i] & 0xffffffffu);
+  atomicAdd(&cnt[keys[i] >> 32], 1);
+}
+
 // ---------------------------------------------------------------- host helpers
 
 void sort_edges(Topology& t, DBuf<int32_t>& eu, DBuf<int32_t>& ev, DBuf<double>& cost) {
@@ -290,6 +446,133 @@ void identity_perm(Topology& t) {
   }
 }
 
+// v2 sweep structures: halo lists, per-slot local indices, CTA adjacency, smem plan.
+static void build_local_index(Topology& t) {
+  cudaStream_t s = t.stream;
+  const int n = t.n, G = t.sweep_ctas;
+  t.v2 = false;
+  t.resident = false;
+  if (n == 0 || t.nslices == 0) return;
+  DBuf<int32_t> cos(t.nslices, s);
+  k_cta_of_slice<<<G, 128, 0, s>>>(G, t.cta_lo.get(), cos.get());
+  launched("cta_of_slice");
+  const int64_t slots = t.sell_slots;
+  // halo entries
+  DBuf<uint64_t> k0(std::max<int64_t>(slots, 1), s), k1(std::max<int64_t>(slots, 1), s);
+  DBuf<int64_t> nsel(1, s);
+  int64_t h = 0;
+  if (slots > 0) {
+    k_halo_keys<<<grid_for(t.nslices * 32, 256), 256, 0, s>>>(n, t.nslices, t.sptr.get(), t.scol.get(),
+                                                             t.seid.get(), cos.get(), t.cta_lo.get(), k0.get());
+    launched("halo_keys");
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), slots, 0, 64, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), slots, 0, 64, s));
+    launched("sort_halo");
+    tmp = 0;
+    F2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, k1.get(), k0.get(), nsel.get(), slots, s));
+    DBuf<char> tb2(tmp, s);
+    F2M_CUDA(cub::DeviceSelect::Unique(tb2.get(), tmp, k1.get(), k0.get(), nsel.get(), slots, s));
+    launched("unique_halo");
+    F2M_CUDA(cudaMemcpyAsync(&h, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    uint64_t last = 0;
+    if (h > 0) {
+      F2M_CUDA(cudaMemcpy(&last, k0.get() + h - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+      if (last == ~0ULL) --h;  // drop the "not halo" sentinel
+    }
+  }
+  t.halo.alloc(std::max<int64_t>(h, 1), s);
+  t.halo_off.alloc(G + 1, s);
+  {
+    DBuf<int32_t> cnt(G + 1, s);
+    F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (G + 1), s));
+    if (h > 0) {
+      k_halo_split<<<grid_for(h, 256), 256, 0, s>>>(h, k0.get(), t.halo.get(), cnt.get());
+      launched("halo_split");
+    }
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.halo_off.get(), G + 1, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.halo_off.get(), G + 1, s));
+    launched("scan_halo");
+  }
+  // sizes
+  {
+    DBuf<int> ml(1, s);
+    DBuf<unsigned long long> ms(1, s);
+    F2M_CUDA(cudaMemsetAsync(ml.get(), 0, sizeof(int), s));
+    F2M_CUDA(cudaMemsetAsync(ms.get(), 0, sizeof(unsigned long long), s));
+    k_local_sizes<<<grid_for(G, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.halo_off.get(), t.sptr.get(), ml.get(),
+                                                   ms.get());
+    launched("local_sizes");
+    int hml = 0;
+    unsigned long long hms = 0;
+    F2M_CUDA(cudaMemcpyAsync(&hml, ml.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(&hms, ms.get(), sizeof(hms), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    t.max_local = hml;
+    t.max_cta_slots = (int64_t)hms;
+  }
+  const size_t limit = sweep_smem_limit(t.dev);
+  const size_t lam_bytes = (size_t)t.max_local * sizeof(double);
+  if (t.max_local > 65535 || lam_bytes > limit) return;  // v1 kernel (global gathers)
+  // per-slot local indices
+  t.slidx.alloc(std::max<int64_t>(slots, 1), s);
+  if (slots > 0) {
+    k_slot_lidx<<<grid_for(t.nslices * 32, 256), 256, 0, s>>>(n, t.nslices, t.sptr.get(), t.scol.get(), t.seid.get(),
+                                                             cos.get(), t.cta_lo.get(), t.halo_off.get(),
+                                                             t.halo.get(), t.slidx.get());
+    launched("slot_lidx");
+  }
+  // CTA adjacency
+  t.nbr_off.alloc(G + 1, s);
+  {
+    DBuf<uint64_t> nk(std::max<int64_t>(h, 1), s), nk2(std::max<int64_t>(h, 1), s);
+    int64_t k = 0;
+    if (h > 0) {
+      k_nbr_keys<<<G, 128, 0, s>>>(G, t.halo_off.get(), t.halo.get(), cos.get(), nk.get());
+      launched("nbr_keys");
+      size_t tmp = 0;
+      F2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, nk.get(), nk2.get(), nsel.get(), h, s));
+      DBuf<char> tb(tmp, s);
+      F2M_CUDA(cub::DeviceSelect::Unique(tb.get(), tmp, nk.get(), nk2.get(), nsel.get(), h, s));
+      launched("unique_nbr");
+      F2M_CUDA(cudaMemcpyAsync(&k, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      F2M_CUDA(cudaStreamSynchronize(s));
+    }
+    t.nbr.alloc(std::max<int64_t>(k, 1), s);
+    DBuf<int32_t> cnt(G + 1, s);
+    F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (G + 1), s));
+    if (k > 0) {
+      k_nbr_split<<<grid_for(k, 256), 256, 0, s>>>(k, nk2.get(), t.nbr.get(), cnt.get());
+      launched("nbr_split");
+    }
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.nbr_off.get(), G + 1, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.nbr_off.get(), G + 1, s));
+    launched("scan_nbr");
+  }
+  // [lam regions][halo ids (<= max_local ints)][resident: cost + local index per slot]
+  const size_t lam_aligned = (lam_bytes + 15) & ~size_t(15);
+  const size_t ids_bytes = (size_t)(lam_aligned / sizeof(double)) * sizeof(int);
+  const size_t resident_bytes =
+      2 * lam_aligned + ids_bytes + (size_t)t.max_cta_slots * (sizeof(double) + sizeof(uint16_t));
+  const size_t streaming_bytes = lam_aligned + ids_bytes;
+  if (streaming_bytes > limit) return;  // v1 kernel
+  // The v3 kernel keeps per-sweep CTA maxima in a ring of 64. A CTA starts sweep s only after
+  // its own convergence helper has seen EVERY CTA publish sweep s-7, so no CTA runs more than
+  // ~16 sweeps ahead of any helper still reading the ring: 64 slots are race-free. The helper
+  // polls up to 256 CTAs per batch.
+  if (G > 256) return;  // v1 kernel
+  t.v2 = true;
+  t.resident = resident_bytes <= limit;
+  t.smem_bytes = t.resident ? resident_bytes : streaming_bytes;
+  F2M_CUDA(cudaStreamSynchronize(s));
+}
+
 void finalize_topology(Topology& t) {
   cudaStream_t s = t.stream;
   const int n = t.n;
@@ -299,6 +582,58 @@ void finalize_topology(Topology& t) {
   if (m > 0) {
     k_degrees<<<grid_for(m, 256), 256, 0, s>>>(m, t.eu.get(), t.ev.get(), t.perm.get(), t.deg.get());
     launched("degrees");
+  }
+  // CTA partition (contiguous slice ranges balanced by degree + a per-slice constant), then
+  // a CTA-local order: interior nodes first, boundary nodes last, each by descending degree
+  // (small SELL padding). The partition is fixed before the reorder, which stays inside ranges.
+  t.nslices = (n + 31) / 32;
+  t.sweep_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sweep_grid_ctas(t.dev), t.nslices));
+  const int G = t.sweep_ctas;
+  t.cta_lo.alloc(G + 1, s);
+  t.cta_int_hi.alloc(G, s);
+  if (n > 0) {
+    DBuf<int64_t> w(t.nslices + 1, s), wp(t.nslices + 1, s);
+    k_slice_weight<<<grid_for(t.nslices, 256), 256, 0, s>>>(n, t.nslices, t.deg.get(), w.get());
+    launched("slice_weight");
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, w.get(), wp.get(), t.nslices + 1, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, w.get(), wp.get(), t.nslices + 1, s));
+    launched("scan_weight");
+    k_partition<<<grid_for(G + 1, 128), 128, 0, s>>>(G, t.nslices, wp.get(), t.cta_lo.get());
+    launched("partition");
+    DBuf<int32_t> cos(t.nslices, s);
+    k_cta_of_slice<<<G, 128, 0, s>>>(G, t.cta_lo.get(), cos.get());
+    launched("cta_of_slice");
+    DBuf<uint8_t> bnd(n, s);
+    F2M_CUDA(cudaMemsetAsync(bnd.get(), 0, n, s));
+    if (m > 0) {
+      k_boundary<<<grid_for(m, 256), 256, 0, s>>>(m, t.eu.get(), t.ev.get(), t.perm.get(), cos.get(), bnd.get());
+      launched("boundary");
+    }
+    DBuf<uint64_t> k0(n, s), k1(n, s);
+    DBuf<int32_t> v0(n, s), v1(n, s), deg2(n, s), ip2(n, s), p2(n, s), nint(G, s);
+    F2M_CUDA(cudaMemsetAsync(nint.get(), 0, sizeof(int32_t) * G, s));
+    k_local_keys<<<grid_for(n, 256), 256, 0, s>>>(n, t.deg.get(), bnd.get(), cos.get(), k0.get(), v0.get(),
+                                                 nint.get());
+    launched("local_keys");
+    tmp = 0;
+    F2M_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.get(), k1.get(), v0.get(), v1.get(), n, 0, 64, s));
+    DBuf<char> tb2(tmp, s);
+    F2M_CUDA(cub::DeviceRadixSort::SortPairs(tb2.get(), tmp, k0.get(), k1.get(), v0.get(), v1.get(), n, 0, 64, s));
+    launched("sort_local");
+    k_window_apply<<<grid_for(n, 256), 256, 0, s>>>(n, v1.get(), t.deg.get(), t.iperm.get(), deg2.get(), ip2.get(),
+                                                   p2.get());
+    launched("local_apply");
+    t.deg = std::move(deg2);
+    t.iperm = std::move(ip2);
+    t.perm = std::move(p2);
+    k_int_hi<<<grid_for(G, 128), 128, 0, s>>>(G, t.cta_lo.get(), nint.get(), t.cta_int_hi.get());
+    launched("int_hi");
+  } else {
+    int zero[2] = {0, 0};
+    F2M_CUDA(cudaMemcpyAsync(t.cta_lo.get(), zero, sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s));
+    F2M_CUDA(cudaMemcpyAsync(t.cta_int_hi.get(), zero, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   }
   // min / max degree
   {
@@ -317,7 +652,6 @@ void finalize_topology(Topology& t) {
     t.max_deg = out[1];
   }
   // SELL-32 layout
-  t.nslices = (n + 31) / 32;
   t.swidth.alloc(t.nslices, s);
   t.sptr.alloc(t.nslices + 1, s);
   DBuf<int64_t> ssize(t.nslices + 1, s);
@@ -353,12 +687,7 @@ void finalize_topology(Topology& t) {
                                                 fill.get(), t.scol.get(), t.seid.get());
     launched("fill_sell");
   }
-  // persistent-sweep CTA partition
-  t.sweep_ctas = sweep_grid_ctas(t.dev);
-  t.cta_lo.alloc(t.sweep_ctas + 1, s);
-  k_partition<<<grid_for(t.sweep_ctas + 1, 128), 128, 0, s>>>(t.sweep_ctas, t.nslices, t.sptr.get(),
-                                                              t.cta_lo.get());
-  launched("partition");
+  build_local_index(t);
 }
 
 double sequential_mean(const double* d_cost, int64_t m, cudaStream_t s) {
@@ -523,6 +852,11 @@ extern "C" int f2m_graph_get_info(const f2m_graph* g, f2m_graph_info* out) {
     out->min_degree = t.min_deg;
     out->max_degree = t.max_deg;
     out->sell_slots = t.sell_slots;
+    out->sweep_ctas = t.sweep_ctas;
+    out->sweep_variant = !t.v2 ? 1 : (t.resident ? 3 : 2);
+    out->max_local = t.max_local;
+    out->max_cta_slots = t.max_cta_slots;
+    out->smem_bytes = (int64_t)t.smem_bytes;
   });
 }
 

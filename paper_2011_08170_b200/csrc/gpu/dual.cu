@@ -19,6 +19,8 @@
 //  k_dual_chunks    dual_objective (dual.cpp:87-123) in the reference's 2048/8192 chunk
 //                   order: one warp per chunk, lane 0 adds in sequence -> bit-exact.
 #include <chrono>
+#include <climits>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -45,6 +47,20 @@ __device__ __forceinline__ void topk_insert(double (&s)[B + 1], double val) {
     }
     s[0] = val < s[0] ? val : s[0];
   }
+}
+
+// Branch-free variant for the sweep kernels: bubble val through the sorted list. A NaN val
+// compares false everywhere and falls off the end, like the guarded insert above.
+template <int B>
+__device__ __forceinline__ void topk_bubble(double (&s)[B + 1], double val) {
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const bool lt = val < s[i];
+    const double lo = lt ? val : s[i];
+    val = lt ? s[i] : val;
+    s[i] = lo;
+  }
+  s[B] = val < s[B] ? val : s[B];
 }
 
 template <int B>
@@ -97,7 +113,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target, int
   __threadfence();
   atomicAdd(bar, 1u);
   const uint64_t t0 = globaltimer_ns();
-  while (ld_acquire_u32(bar) < target) {
+  while (ld_relaxed_u32(bar) < target) {
     if (globaltimer_ns() - t0 > 20ull * 1000000000ull) {  // 20 s watchdog: never hang the GPU
       atomicExch(err, 1);
       break;
@@ -190,6 +206,385 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep(SweepArgs a, Swe
   }
 }
 
+
+// ---------------------------------------------------------------- persistent Jacobi sweep v3
+// Neighbour-synchronised persistent kernel (no grid barrier).
+//  * CTA c owns a contiguous, degree-balanced slice range; inside it interior nodes (all
+//    neighbours in the CTA) come first, boundary nodes last.
+//  * lambda lives in four global buffers (sweep s reads glam[s%4], writes glam[(s+1)%4]) and,
+//    per CTA, in a shared-memory region [own | halo] (two regions, alternating, in resident
+//    mode, so the CTA's own multipliers never round-trip through L2).
+//  * The last warp is the sync warp: it waits until the CTAs owning this CTA's halo nodes
+//    have published sweep s-1 (per-CTA release flags), stages the halo multipliers into
+//    shared memory and signals named barrier 1, while the other 31 warps already update the
+//    interior slices. Boundary slices start after barrier 1.
+//  * Convergence (max|delta| <= eps*mean_cost, dual.cpp:235) of sweep k is evaluated by the
+//    sync warp during sweep k+3 from the CTAs' published maxima and applied at the top of
+//    sweep k+4 — before anything overwrites glam[(k+1)%4], the result of sweep k. All CTAs see
+//    the same maxima, so all stop at the same k; sweeps k+1..k+3 are discarded speculation.
+struct SweepCtl2 {
+  int error;
+  int sweeps;
+  int converged;
+  int out_buffer;
+  double final_max;
+};
+
+struct Sweep3Args {
+  int n;
+  const int64_t* __restrict__ sptr;
+  const int32_t* __restrict__ swidth;
+  const int32_t* __restrict__ cta_lo;
+  const int32_t* __restrict__ cta_int_hi;
+  const uint16_t* __restrict__ slidx;
+  const double* __restrict__ scost;
+  const int32_t* __restrict__ halo_off;
+  const int32_t* __restrict__ halo;
+  const int32_t* __restrict__ nbr_off;
+  const int32_t* __restrict__ nbr;
+  double* glam[8];  // lambda buffers: sweep s reads glam[s%8], writes glam[(s+1)%8]
+  int* flags;       // [G]: sweeps completed by CTA c
+  double* cmax;     // [kCmaxRing][G]: CTA max |delta| per sweep (ring)
+  double eta;
+  int update;
+  double threshold;
+  int max_sweeps;
+  double* record;
+  int lam_stride;  // doubles per shared-memory lambda region (16-byte multiple)
+  // optional phase trace (F2M_SWEEP_TRACE=first,count): globaltimer stamps per (sweep, CTA, phase)
+  unsigned long long* trace;
+  int trace_first, trace_count;
+};
+
+#define F2M_TRACE(S, PH)                                                                    \
+  do {                                                                                      \
+    if (a.trace && (S) >= a.trace_first && (S) < a.trace_first + a.trace_count)             \
+      a.trace[(((size_t)((S) - a.trace_first) * gridDim.x + blockIdx.x) << 3) + (PH)] =      \
+          globaltimer_ns();                                                                 \
+  } while (0)
+
+// one warp: wait until every CTA has published >= target. Loads are issued as a batch (the
+// reduction comes after all of them), so a poll costs one L2 round trip, not ceil(G/32).
+constexpr int kMaxCtaBatch = 8;  // supports G <= 256 CTAs
+__device__ __forceinline__ bool wait_all_ctas(const int* flags, int G, int target, int* err_local) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    int v[kMaxCtaBatch];
+#pragma unroll
+    for (int b = 0; b < kMaxCtaBatch; ++b) {
+      const int i = lane + 32 * b;
+      v[b] = i < G ? ld_relaxed(flags + i) : INT_MAX;
+    }
+    int mn = INT_MAX;
+#pragma unroll
+    for (int b = 0; b < kMaxCtaBatch; ++b) mn = min(mn, v[b]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (mn >= target) break;
+    if (globaltimer_ns() - t0 > 20ull * 1000000000ull) { *err_local = 1; return false; }
+  }
+  fence_acq_rel_gpu();
+  return true;
+}
+
+__device__ __forceinline__ double global_max(const double* v, int G) {
+  const int lane = threadIdx.x & 31;
+  double x[kMaxCtaBatch];
+#pragma unroll
+  for (int b = 0; b < kMaxCtaBatch; ++b) {
+    const int i = lane + 32 * b;
+    x[b] = i < G ? __ldcg(v + i) : 0.0;
+  }
+  double mx = 0.0;
+#pragma unroll
+  for (int b = 0; b < kMaxCtaBatch; ++b) mx = mx < x[b] ? x[b] : mx;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = mx < y ? y : mx;
+  }
+  return mx;
+}
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+constexpr int kLamBufs = 8;     // convergence verdicts may lag the sweeps by up to 7
+constexpr int kCmaxRing = 64;   // CTAs stay within ~16 sweeps of every helper (see core.cu)
+
+__device__ __forceinline__ int vload(const volatile int* p) { return *p; }
+
+template <int B, bool RES>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep3(Sweep3Args a, SweepCtl2* ctl) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[kSweepThreads / 32];
+  __shared__ unsigned long long wstart[kSweepThreads / 32], wfin[kSweepThreads / 32];
+  __shared__ int s_stop, s_err;
+  // helper -> main loop (volatile, no barrier between them)
+  __shared__ int h_done, h_conv, h_exit;
+  __shared__ double h_g, h_gconv;
+  const int c = blockIdx.x, G = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int sync_warp = nwarps - 1, helper_warp = nwarps - 2, ncw = nwarps - 2;
+  const int main_threads = (nwarps - 1) * 32;  // all but the helper warp
+  const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
+  const int p0 = s_lo * 32;
+  const int own = max(0, min(s_hi * 32, a.n) - p0);
+  const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
+  const int nb0 = a.nbr_off[c], nnb = a.nbr_off[c + 1] - nb0;
+  const int64_t slot0 = a.sptr[s_lo];
+  const int nslots = (int)(a.sptr[s_hi] - slot0);
+  // shared memory: [lam A | lam B (resident)] [halo ids] [cost | local index (resident)]
+  double* regA = reinterpret_cast<double*>(smem);
+  double* regB = regA + (RES ? a.lam_stride : 0);
+  int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
+  double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
+  uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
+  const double* __restrict__ gcost = a.scost + slot0;
+  const uint16_t* __restrict__ glid = a.slidx + slot0;
+  for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo[h0 + i];
+  if (RES) {  // the CTA's slot data and own multipliers stay in shared memory for the whole solve
+    for (int i = tid; i < nslots; i += blockDim.x) {
+      cst_s[i] = gcost[i];
+      lid_s[i] = glid[i];
+    }
+    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.glam[0][p0 + i];
+  }
+  if (tid < kSweepThreads / 32) wstart[tid] = wfin[tid] = 0;
+  if (tid == 0) {
+    s_err = 0;
+    h_done = 0;
+    h_conv = -1;
+    h_exit = 0;
+    h_g = INFINITY;
+    h_gconv = INFINITY;
+  }
+  __syncthreads();
+
+  if (warp == helper_warp) {
+    // ---- convergence helper: verdict on sweep k once every CTA has published it
+    // (max|delta| <= eps*mean_cost, dual.cpp:235). Runs beside the sweeps, never in their way.
+    for (int k = 0; k < a.max_sweeps; ++k) {
+      const uint64_t t0 = globaltimer_ns();
+      bool ready = false;
+      while (!ready) {
+        int v[kMaxCtaBatch];
+#pragma unroll
+        for (int b = 0; b < kMaxCtaBatch; ++b) {
+          const int i = lane + 32 * b;
+          v[b] = i < G ? ld_relaxed(a.flags + i) : INT_MAX;
+        }
+        int mn = INT_MAX;
+#pragma unroll
+        for (int b = 0; b < kMaxCtaBatch; ++b) mn = min(mn, v[b]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        ready = mn >= k + 1;
+        if (!ready && (vload(&h_exit) || globaltimer_ns() - t0 > 20ull * 1000000000ull)) break;
+      }
+      if (!ready) {
+        if (!vload(&h_exit) && lane == 0) s_err = 1;
+        break;
+      }
+      fence_acq_rel_gpu();
+      const double g = global_max(a.cmax + (size_t)(k % kCmaxRing) * G, G);
+      if (lane == 0) {
+        if (c == 0 && a.record) a.record[k] = g;
+        h_g = g;
+        if (g <= a.threshold) {
+          h_gconv = g;
+          h_conv = k;
+        }
+        __threadfence_block();
+        h_done = k + 1;
+      }
+      __syncwarp();
+      if (g <= a.threshold) break;
+    }
+  } else {
+    // ---- main loop: 30 compute warps + the sync warp
+    for (int s = 0;; ++s) {
+      if (warp == 0 && lane == 0) {
+        int decided = -1;
+        // every verdict for k <= s - kLamBufs must be in before sweep s overwrites glam[(s+1)%8]
+        while (vload(&h_done) < s - kLamBufs + 1 && vload(&h_conv) < 0 && !vload(&s_err)) {
+        }
+        if (vload(&h_conv) >= 0) decided = vload(&h_conv);
+        else if (s >= a.max_sweeps) {
+          while (vload(&h_done) < a.max_sweeps && vload(&h_conv) < 0 && !vload(&s_err)) {
+          }
+          decided = vload(&h_conv) >= 0 ? vload(&h_conv) : a.max_sweeps - 1;
+        }
+        if (vload(&s_err)) decided = max(s - 1, 0);
+        s_stop = decided;
+      }
+      named_sync(2, main_threads);  // [A]
+      if (s_stop >= 0) break;
+      if (tid == 0) F2M_TRACE(s, 0);
+      double* lam = (RES && (s & 1)) ? regB : regA;
+      double* lam_next = (s & 1) ? regA : regB;
+      const double* gin = a.glam[s & 7];
+      double* gout = a.glam[(s + 1) & 7];
+      if (!RES) {  // stage own multipliers (written by this CTA last sweep)
+        for (int i = tid; i < own; i += main_threads) lam[i] = __ldcg(gin + p0 + i);
+        named_sync(2, main_threads);
+      }
+      double mx = 0.0;
+      if (warp == sync_warp) {
+        if (s >= 1) {  // halo owners have published sweep s-1 (or a verdict ended the solve)
+          const uint64_t t0 = globaltimer_ns();
+          for (;;) {
+            bool ok = true;
+            for (int i = lane; i < nnb; i += 32) ok &= ld_relaxed(a.flags + a.nbr[nb0 + i]) >= s;
+            if (__all_sync(0xffffffffu, ok)) break;
+            if (vload(&h_conv) >= 0) break;
+            if (globaltimer_ns() - t0 > 20ull * 1000000000ull) { s_err = 1; break; }
+          }
+          fence_acq_rel_gpu();
+        }
+        if (lane == 0) F2M_TRACE(s, 1);
+        for (int base = 0; base < nh; base += 32 * 8) {  // batched gathers: ~1 round trip
+          double v[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const int i = base + lane + 32 * b;
+            v[b] = i < nh ? __ldcg(gin + halo_s[i]) : 0.0;
+          }
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const int i = base + lane + 32 * b;
+            if (i < nh) lam[own + i] = v[b];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) F2M_TRACE(s, 2);
+        named_arrive(1, main_threads);  // arrive orders this warp's smem writes for bar.sync
+      } else {
+        bool halo_ready = false;
+        for (int sl = s_lo + warp; sl < s_hi; sl += ncw) {
+          if (!halo_ready && sl >= s_int) {
+            named_sync(1, main_threads);
+            halo_ready = true;
+            if (a.trace && lane == 0) wstart[warp] = globaltimer_ns();
+          }
+          const int p = sl * 32 + lane;
+          if (p >= a.n) continue;
+          const int lp = p - p0;
+          const int lb = (int)(a.sptr[sl] - slot0) + lane;
+          const int w = a.swidth[sl];
+          const double lv = lam[lp];
+          double sv[B + 1];
+#pragma unroll
+          for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
+          int j = 0;
+          for (; j + 8 <= w; j += 8) {  // 8 slots in flight per thread
+            int li[8];
+            double cs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int idx = lb + 32 * (j + u);
+              li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
+              cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+          }
+          for (; j < w; ++j) {
+            const int idx = lb + 32 * j;
+            const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
+            const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
+            topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
+          }
+          const double d = delta_of<B>(sv, a.update);
+          const double nl = dadd(lv, dmul(a.eta, d));
+          gout[p] = nl;
+          if (RES) lam_next[lp] = nl;
+          const double ad = fabs(d);
+          mx = mx < ad ? ad : mx;
+        }
+        if (warp == 0 && lane == 0) F2M_TRACE(s, 4);
+        if (a.trace && lane == 0) wfin[warp] = globaltimer_ns();
+        if (!halo_ready) named_sync(1, main_threads);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = mx < o ? o : mx;
+      }
+      if (lane == 0) red[warp] = mx;
+      named_sync(2, main_threads);  // [B]
+      if (tid == 0) F2M_TRACE(s, 5);
+      if (a.trace && tid == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count) {
+        unsigned long long bmin = ~0ULL, fmax = 0;
+        for (int w = 0; w < ncw; ++w) {
+          if (wstart[w] && wstart[w] < bmin) bmin = wstart[w];
+          if (wfin[w] > fmax) fmax = wfin[w];
+          wstart[w] = 0;
+        }
+        const size_t o = (((size_t)(s - a.trace_first) * gridDim.x + blockIdx.x) << 3);
+        a.trace[o + 3] = bmin == ~0ULL ? 0 : bmin;
+        a.trace[o + 7] = fmax;
+      }
+      if (warp == 0) {
+        double bm = (lane < nwarps && lane != helper_warp) ? red[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          const double o = __shfl_xor_sync(0xffffffffu, bm, off);
+          bm = bm < o ? o : bm;
+        }
+        if (lane == 0) {
+          a.cmax[(size_t)(s % kCmaxRing) * G + c] = bm;
+          // release (cumulative over the CTA's writes ordered before it by the barrier)
+          st_release(a.flags + c, s + 1);
+          F2M_TRACE(s, 6);
+        }
+      }
+    }
+    if (tid == 0) h_exit = 1;
+  }
+  __syncthreads();
+  if (tid == 0 && s_err) atomicExch(&ctl->error, 1);
+  if (c == 0 && tid == 0) {
+    const int k = s_stop;
+    ctl->sweeps = k + 1;
+    ctl->converged = h_conv >= 0 ? 1 : 0;
+    ctl->final_max = h_conv >= 0 ? h_gconv : h_g;
+    ctl->out_buffer = (k + 1) & 7;
+  }
+}
+
+size_t sweep_smem_limit(int dev) {
+  const cudaDeviceProp& p = device_props(dev);
+  return p.sharedMemPerBlockOptin > 4096 ? p.sharedMemPerBlockOptin - 4096 : 0;
+}
+
+template <int B, bool RES>
+static void launch_sweep2(const Sweep3Args& a, SweepCtl2* ctl, int ctas, size_t smem, cudaStream_t s) {
+  auto fn = k_gdp_sweep3<B, RES>;
+  F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&a, (void*)&ctl};
+  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kSweepThreads), args, smem, s));
+}
+
+template <bool RES>
+static void dispatch_sweep2(int b, const Sweep3Args& a, SweepCtl2* ctl, int ctas, size_t smem, cudaStream_t s) {
+  switch (b) {
+    case 1: launch_sweep2<1, RES>(a, ctl, ctas, smem, s); break;
+    case 2: launch_sweep2<2, RES>(a, ctl, ctas, smem, s); break;
+    case 3: launch_sweep2<3, RES>(a, ctl, ctas, smem, s); break;
+    case 4: launch_sweep2<4, RES>(a, ctl, ctas, smem, s); break;
+    case 5: launch_sweep2<5, RES>(a, ctl, ctas, smem, s); break;
+    case 6: launch_sweep2<6, RES>(a, ctl, ctas, smem, s); break;
+    case 7: launch_sweep2<7, RES>(a, ctl, ctas, smem, s); break;
+    default: launch_sweep2<8, RES>(a, ctl, ctas, smem, s); break;
+  }
+}
+
 static double g_last_sweep_ms = 0.0;
 static int g_last_sweep_count = 0;
 
@@ -200,58 +595,146 @@ static void launch_sweep(const SweepArgs& a, SweepCtl* ctl, int ctas, cudaStream
                                        args, 0, s));
 }
 
+static int g_force_v1 = -1;  // F2M_SWEEP_V1=1 forces the grid-barrier kernel (A/B testing)
+
+static bool use_v1(const Topology& t) {
+  if (g_force_v1 < 0) {
+    const char* e = std::getenv("F2M_SWEEP_V1");
+    g_force_v1 = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_force_v1 == 1 || !t.v2;
+}
+
 SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam0,
                        double* d_lam1, int max_sweeps, double threshold, double* d_record) {
   const Topology& t = *g.topo;
   cudaStream_t s = t.stream;
   SweepResult r;
   if (max_sweeps <= 0) return r;
-  DBuf<SweepCtl> ctl(1, s);
-  F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl), s));
-  SweepArgs a;
-  a.n = t.n;
-  a.sptr = t.sptr.get();
-  a.swidth = t.swidth.get();
-  a.scol = t.scol.get();
-  a.scost = g.scost.get();
-  a.cta_lo = t.cta_lo.get();
-  a.lam0 = d_lam0;
-  a.lam1 = d_lam1;
-  a.eta = cfg.eta;
-  a.update = cfg.update;
-  a.threshold = threshold;
-  a.max_sweeps = max_sweeps;
-  a.record = d_record;
   cudaEvent_t e0, e1;
   F2M_CUDA(cudaEventCreate(&e0));
   F2M_CUDA(cudaEventCreate(&e1));
-  F2M_CUDA(cudaEventRecord(e0, s));
-  switch (cfg.b) {
-    case 1: launch_sweep<1>(a, ctl.get(), t.sweep_ctas, s); break;
-    case 2: launch_sweep<2>(a, ctl.get(), t.sweep_ctas, s); break;
-    case 3: launch_sweep<3>(a, ctl.get(), t.sweep_ctas, s); break;
-    case 4: launch_sweep<4>(a, ctl.get(), t.sweep_ctas, s); break;
-    case 5: launch_sweep<5>(a, ctl.get(), t.sweep_ctas, s); break;
-    case 6: launch_sweep<6>(a, ctl.get(), t.sweep_ctas, s); break;
-    case 7: launch_sweep<7>(a, ctl.get(), t.sweep_ctas, s); break;
-    default: launch_sweep<8>(a, ctl.get(), t.sweep_ctas, s); break;
+  int error = 0, sweeps = 0, converged = 0, outbuf = 0;
+  double final_max = INFINITY;
+  if (use_v1(t)) {
+    DBuf<SweepCtl> ctl(1, s);
+    F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl), s));
+    SweepArgs a;
+    a.n = t.n;
+    a.sptr = t.sptr.get();
+    a.swidth = t.swidth.get();
+    a.scol = t.scol.get();
+    a.scost = g.scost.get();
+    a.cta_lo = t.cta_lo.get();
+    a.lam0 = d_lam0;
+    a.lam1 = d_lam1;
+    a.eta = cfg.eta;
+    a.update = cfg.update;
+    a.threshold = threshold;
+    a.max_sweeps = max_sweeps;
+    a.record = d_record;
+    F2M_CUDA(cudaEventRecord(e0, s));
+    switch (cfg.b) {
+      case 1: launch_sweep<1>(a, ctl.get(), t.sweep_ctas, s); break;
+      case 2: launch_sweep<2>(a, ctl.get(), t.sweep_ctas, s); break;
+      case 3: launch_sweep<3>(a, ctl.get(), t.sweep_ctas, s); break;
+      case 4: launch_sweep<4>(a, ctl.get(), t.sweep_ctas, s); break;
+      case 5: launch_sweep<5>(a, ctl.get(), t.sweep_ctas, s); break;
+      case 6: launch_sweep<6>(a, ctl.get(), t.sweep_ctas, s); break;
+      case 7: launch_sweep<7>(a, ctl.get(), t.sweep_ctas, s); break;
+      default: launch_sweep<8>(a, ctl.get(), t.sweep_ctas, s); break;
+    }
+    launched("gdp_sweep");
+    F2M_CUDA(cudaEventRecord(e1, s));
+    SweepCtl h;
+    F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    error = h.error;
+    sweeps = h.sweeps;
+    converged = h.converged;
+    final_max = h.final_max;
+    outbuf = (h.sweeps & 1) ? 1 : 0;
+  } else {
+    const int G = t.sweep_ctas;
+    DBuf<double> extra((size_t)6 * std::max(t.n, 1), s);
+    DBuf<SweepCtl2> ctl(1, s);
+    DBuf<int> flags(G, s);
+    DBuf<double> cmax((size_t)kCmaxRing * G, s);
+    F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl2), s));
+    F2M_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * G, s));
+    Sweep3Args a;
+    a.n = t.n;
+    a.sptr = t.sptr.get();
+    a.swidth = t.swidth.get();
+    a.cta_lo = t.cta_lo.get();
+    a.cta_int_hi = t.cta_int_hi.get();
+    a.slidx = t.slidx.get();
+    a.scost = g.scost.get();
+    a.halo_off = t.halo_off.get();
+    a.halo = t.halo.get();
+    a.nbr_off = t.nbr_off.get();
+    a.nbr = t.nbr.get();
+    a.glam[0] = d_lam0;
+    a.glam[1] = d_lam1;
+    for (int i = 2; i < kLamBufs; ++i) a.glam[i] = extra.get() + (size_t)(i - 2) * std::max(t.n, 1);
+    a.flags = flags.get();
+    a.cmax = cmax.get();
+    a.eta = cfg.eta;
+    a.update = cfg.update;
+    a.threshold = threshold;
+    a.max_sweeps = max_sweeps;
+    a.record = d_record;
+    a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.trace = nullptr;
+    a.trace_first = a.trace_count = 0;
+    DBuf<unsigned long long> trace;
+    if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {  // "first,count" -> f2m_sweep_trace.bin
+      std::sscanf(tr, "%d,%d", &a.trace_first, &a.trace_count);
+      if (a.trace_count > 0) {
+        trace.alloc((size_t)a.trace_count * G * 8, s);
+        F2M_CUDA(cudaMemsetAsync(trace.get(), 0, trace.bytes(), s));
+        a.trace = trace.get();
+      }
+    }
+    F2M_CUDA(cudaEventRecord(e0, s));
+    if (t.resident) dispatch_sweep2<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+    else dispatch_sweep2<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+    launched("gdp_sweep3");
+    F2M_CUDA(cudaEventRecord(e1, s));
+    SweepCtl2 h;
+    F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    error = h.error;
+    sweeps = h.sweeps;
+    converged = h.converged;
+    final_max = h.final_max;
+    outbuf = h.out_buffer;
+    if (outbuf >= 2 && t.n > 0)  // hand the result back in one of the caller's two buffers
+      F2M_CUDA(cudaMemcpyAsync(d_lam1, a.glam[outbuf], sizeof(double) * t.n, cudaMemcpyDeviceToDevice, s));
+    if (outbuf >= 2) outbuf = 1;
+    F2M_CUDA(cudaStreamSynchronize(s));
+    if (a.trace) {
+      std::vector<unsigned long long> hbuf(trace.n);
+      F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
+      if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
+        const int hdr[3] = {a.trace_first, a.trace_count, G};
+        std::fwrite(hdr, sizeof(int), 3, f);
+        std::fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
+        std::fclose(f);
+      }
+    }
   }
-  launched("gdp_sweep");
-  F2M_CUDA(cudaEventRecord(e1, s));
-  SweepCtl h;
-  F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   g_last_sweep_ms = ms;
-  g_last_sweep_count = h.sweeps;
-  if (h.error) throw Error(F2M_E_TIMEOUT, "gdp sweep kernel: grid barrier watchdog fired");
-  r.sweeps = h.sweeps;
-  r.converged = h.converged;
-  r.final_max_abs_delta = h.final_max;
-  r.out_buffer = (h.sweeps & 1) ? 1 : 0;
+  g_last_sweep_count = sweeps;
+  if (error) throw Error(F2M_E_TIMEOUT, "gdp sweep kernel: synchronisation watchdog fired");
+  r.sweeps = sweeps;
+  r.converged = converged;
+  r.final_max_abs_delta = final_max;
+  r.out_buffer = outbuf;
   return r;
 }
 
@@ -280,9 +763,10 @@ __global__ void __launch_bounds__(256) k_init_local_midpoint(
       double other = 0.0;  // lambda of a higher-numbered (or the same) node is still 0
       if (iperm[q] < v) {
         const uint64_t t0 = globaltimer_ns();
-        while (ld_acquire(done + q) == 0) {
+        while (ld_relaxed(done + q) == 0) {
           if (globaltimer_ns() - t0 > 20ull * 1000000000ull) { atomicExch(err, 1); break; }
         }
+        fence_acq_rel_gpu();
         other = __ldcg(lam + q);
       }
       // ge.cost - lv - other with lv = lambda[v] = 0 (dual.cpp:43)

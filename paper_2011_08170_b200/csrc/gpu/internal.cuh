@@ -132,6 +132,22 @@ struct Topology {
   // persistent-sweep partition: CTA c owns slices [cta_lo[c], cta_lo[c+1])
   int sweep_ctas = 0;
   DBuf<int32_t> cta_lo;        // [sweep_ctas+1]
+  DBuf<int32_t> cta_int_hi;    // [sweep_ctas]: slices [cta_lo[c], cta_int_hi[c]) hold only interior
+                               // nodes (no neighbour outside the CTA); boundary nodes follow
+  // v2 sweep (neighbour-flag synchronised): per-CTA local index space. Local index li of
+  // CTA c: li < own_c -> position p0_c + li; else halo[halo_off[c] + li - own_c]. Every slot
+  // also carries its neighbour's local index (slidx, uint16), so a sweep gathers each distinct
+  // lambda once into shared memory and all slot reads hit shared memory.
+  bool v2 = false;             // local index space built (max local count <= 65535)
+  bool resident = false;       // per-CTA slot data (cost + slidx) fits in shared memory
+  DBuf<int32_t> halo_off;      // [ctas+1]
+  DBuf<int32_t> halo;          // positions (sorted per CTA)
+  DBuf<uint16_t> slidx;        // [sell_slots]
+  DBuf<int32_t> nbr_off;       // [ctas+1] CTA adjacency (owners of halo nodes)
+  DBuf<int32_t> nbr;
+  int max_local = 0;           // max over CTAs of own + halo
+  int64_t max_cta_slots = 0;   // max over CTAs of padded slots
+  size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
   ~Topology();
 };
 
@@ -201,6 +217,7 @@ void verify_device(const f2m_graph& g, const double* d_x, double objective,
 // persistent sweep launch geometry (dual.cu)
 int sweep_grid_ctas(int dev);
 int sweep_block_threads();
+size_t sweep_smem_limit(int dev);
 
 // knn.cu
 // xy: device pointer, or host pointer when xy_on_host (staged on the graph's own stream).
@@ -237,6 +254,19 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Polling loads are relaxed (an ld.acquire.gpu compiles to LDG.STRONG + CCTL.IVALL, an L1
+// invalidation per poll); once the condition holds, one acquire fence orders what follows.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -158,7 +158,16 @@ PYBIND11_MODULE(_f2m, m) {
              f2m::check(f2m_graph_get_info(g.handle(), &info));
              return info.sell_slots;
            })
-      .def("sweep_bytes", [](const f2m::Graph& g) { return f2m_sweep_algorithmic_bytes(g.handle()); });
+      .def("sweep_bytes", [](const f2m::Graph& g) { return f2m_sweep_algorithmic_bytes(g.handle()); })
+      .def("layout", [](const f2m::Graph& g) {
+        f2m_graph_info i{};
+        f2m::check(f2m_graph_get_info(g.handle(), &i));
+        return py::dict(py::arg("n") = i.n, py::arg("m") = i.m, py::arg("sell_slots") = i.sell_slots,
+                        py::arg("min_degree") = i.min_degree, py::arg("max_degree") = i.max_degree,
+                        py::arg("sweep_ctas") = i.sweep_ctas, py::arg("sweep_variant") = i.sweep_variant,
+                        py::arg("max_local") = i.max_local, py::arg("max_cta_slots") = i.max_cta_slots,
+                        py::arg("smem_bytes") = i.smem_bytes);
+      });
 
   m.def(
       "build_knn_graph",

@@ -48,6 +48,13 @@ CASES = {
                                  "1e-8", "--max-sweeps", "200000", "--seed", "7", "--sweeps", "3"],
                                 False, True),
     "u100k_s1": (["--synthetic", "100000", "1", "1000", "--k", "10", "--sweeps", "3"], False, True),
+    # config 4 family: clustered instances from paper_2011_08170_b200.generate_clustered_instance
+    # (the reference has no clustered generator; points are passed to it exactly)
+    "clust20k_s1": (["--clustered", "20000", "1", "--k", "10", "--sweeps", "5"], False, True),
+    "u200k_s1": (["--synthetic", "200000", "1", "1000", "--k", "10", "--max-sweeps", "200000",
+                  "--full-only"], False, True),
+    "clust200k_s1": (["--clustered", "200000", "1", "--k", "10", "--max-sweeps", "200000",
+                      "--full-only"], False, True),
 }
 # bucketed == quadratic scan grid of test_graph.cpp:39-50 (rounded mode = heavy ties)
 for _seed in (1, 2, 3):
@@ -63,9 +70,23 @@ def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
+def _expand(args, d):
+    """--clustered N SEED -> --points FILE written by the B200 package's host generator."""
+    if "--clustered" not in args:
+        return args
+    i = args.index("--clustered")
+    n, seed = int(args[i + 1]), int(args[i + 2])
+    sys.path.insert(0, ROOT)
+    import paper_2011_08170_b200 as f2m
+    pts = f2m.generate_clustered_instance(n, seed).points_array()
+    path = os.path.join(d, "in_points.f64")
+    pts.astype(np.float64).tofile(path)
+    return args[:i] + ["--points", path] + args[i + 3:]
+
+
 def run_case(name: str, args, keep: bool) -> None:
     with tempfile.TemporaryDirectory() as d:
-        subprocess.check_call([DUMP, d] + args)
+        subprocess.check_call([DUMP, d] + _expand(args, d))
         meta = json.load(open(os.path.join(d, "meta.json")))
         arrays = {}
         for fn, dt in (("eu.i32", np.int32), ("ev.i32", np.int32), ("ec.f64", np.float64),

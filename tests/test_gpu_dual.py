@@ -233,3 +233,26 @@ def test_local_update_contract(f2m):
             vals = sorted(c - t[a] - t[b] for a, b, c in edges if a == v or b == v)
             assert abs(vals[1] + vals[2]) <= 1e-12
             assert vals[1] <= 1e-12 and vals[2] >= -1e-12
+
+
+def test_grid_barrier_kernel_fallback_parity():
+    """The v1 grid-barrier sweep kernel (used when a CTA's local index space exceeds 16 bits or
+    shared memory) stays bit-exact: run it in a subprocess with F2M_SWEEP_V1=1."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys, json, hashlib, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2011_08170_b200 as f2m\n"
+        "g = f2m.build_knn_graph(f2m.generate_instance(10000, 1, 1000.0), 10)\n"
+        "st, rep = f2m.solve_duals(g)\n"
+        "print(json.dumps([rep['sweeps'], rep['dual_value'], hashlib.sha256(np.array(st.lam).tobytes()).hexdigest()]))\n"
+    ) % (ROOT, os.path.join(ROOT, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, F2M_SWEEP_V1="1"),
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    sweeps, dual, digest = json.loads(out.stdout.strip().splitlines()[-1])
+    meta, _ = golden("u10k_s1")
+    assert sweeps == meta["sweeps"] and dual == meta["dual_value"] and digest == meta["sha256"]["lam_final"]

@@ -5,6 +5,7 @@ import numpy as np
 import paper_2011_08170_b200 as f2m
 print(f2m.device_info(), flush=True)
 for n, seed in ((10000, 1), (100000, 1), (200000, 1)):
+    print(f2m.build_knn_graph(f2m.generate_instance(n, seed), 10).layout(), flush=True)
     inst = f2m.generate_instance(n, seed)
     xy = inst.points_array()
     for rep in range(2):

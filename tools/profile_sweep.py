@@ -8,6 +8,7 @@ import paper_2011_08170_b200 as f2m  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 g = f2m.build_knn_graph(f2m.generate_instance(n, 1), 10)
+print(g.layout())
 st = f2m.make_initial_state(g)
 mx, dv = f2m.jacobi_sweeps(g, st, sweeps)
 ms, sw = f2m.last_sweep_kernel()
