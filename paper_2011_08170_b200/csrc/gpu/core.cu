@@ -38,7 +38,7 @@ Topology::~Topology() {
     eu.release(); ev.release(); perm.release(); iperm.release(); deg.release();
     sptr.release(); swidth.release(); scol.release(); seid.release(); cta_lo.release();
     halo_off.release(); halo.release(); slidx.release(); nbr_off.release(); nbr.release();
-    cta_int_hi.release();
+    cta_int_hi.release(); cta_nint.release(); boff.release(); halo_pub.release();
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
@@ -408,6 +408,27 @@ __global__ void k_nbr_split(int64_t k, const uint64_t* __restrict__ keys, int32_
   atomicAdd(&cnt[keys[i] >> 32], 1);
 }
 
+// ---- v4 LL exchange: boundary publication indices
+__global__ void k_boundary_counts(int ctas, int n, const int32_t* __restrict__ lo, const int32_t* __restrict__ nint,
+                                  int32_t* __restrict__ cnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > ctas) return;
+  if (c == ctas) { cnt[c] = 0; return; }
+  int p0, p1;
+  own_range(c, n, lo, p0, p1);
+  cnt[c] = max(0, (p1 - p0) - nint[c]);
+}
+
+__global__ void k_halo_pub(int64_t h, const int32_t* __restrict__ halo, const int32_t* __restrict__ cos,
+                           const int32_t* __restrict__ lo, const int32_t* __restrict__ nint,
+                           const int32_t* __restrict__ boff, int32_t* __restrict__ pub) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= h) return;
+  const int q = halo[i];
+  const int c = cos[q >> 5];
+  pub[i] = boff[c] + (q - lo[c] * 32 - nint[c]);  // q is a boundary node of its owner (symmetric graph)
+}
+
 // ---------------------------------------------------------------- host helpers
 
 void sort_edges(Topology& t, DBuf<int32_t>& eu, DBuf<int32_t>& ev, DBuf<double>& cost) {
@@ -555,6 +576,26 @@ static void build_local_index(Topology& t) {
     F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.nbr_off.get(), G + 1, s));
     launched("scan_nbr");
   }
+  // v4 LL publication indices (boundary nodes of each CTA, in position order)
+  t.boff.alloc(G + 1, s);
+  t.halo_pub.alloc(std::max<int64_t>(h, 1), s);
+  {
+    DBuf<int32_t> cnt(G + 1, s);
+    k_boundary_counts<<<grid_for(G + 1, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.cta_nint.get(), cnt.get());
+    launched("boundary_counts");
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.boff.get(), G + 1, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.boff.get(), G + 1, s));
+    launched("scan_boundary");
+    if (h > 0) {
+      k_halo_pub<<<grid_for(h, 256), 256, 0, s>>>(h, t.halo.get(), cos.get(), t.cta_lo.get(), t.cta_nint.get(),
+                                                  t.boff.get(), t.halo_pub.get());
+      launched("halo_pub");
+    }
+    F2M_CUDA(cudaMemcpyAsync(&t.nboundary, t.boff.get() + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+  }
   // [lam regions][halo ids (<= max_local ints)][resident: cost + local index per slot]
   const size_t lam_aligned = (lam_bytes + 15) & ~size_t(15);
   const size_t ids_bytes = (size_t)(lam_aligned / sizeof(double)) * sizeof(int);
@@ -630,6 +671,7 @@ void finalize_topology(Topology& t) {
     t.perm = std::move(p2);
     k_int_hi<<<grid_for(G, 128), 128, 0, s>>>(G, t.cta_lo.get(), nint.get(), t.cta_int_hi.get());
     launched("int_hi");
+    t.cta_nint = std::move(nint);
   } else {
     int zero[2] = {0, 0};
     F2M_CUDA(cudaMemcpyAsync(t.cta_lo.get(), zero, sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s));

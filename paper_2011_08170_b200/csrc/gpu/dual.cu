@@ -558,6 +558,791 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep3(Sweep3Args a, S
   }
 }
 
+// ---------------------------------------------------------------- persistent Jacobi sweep v4
+// v3's CTA-local structure (interior-first slices, smem-resident slots and multipliers, a sync
+// warp staging the halo while the other warps update interior nodes) with the inter-CTA traffic
+// moved to an LL ("low-latency") protocol: every published fp64 value travels as two 8-byte
+// words {tag:32 | half:32}, written with one relaxed 16-byte store and polled with one relaxed
+// 16-byte load. A word is single-copy atomic, so a matching tag in both words proves the value is
+// complete — no fences, no flags, one L2 trip from producer to consumer (tools/microbench:
+// LL round trip 0.5-1.1 us vs 1.4-2.6 us for release/acquire flags).
+//  * boundary node p of CTA c publishes lambda after sweep s at ll[(s+1)%kLLRing][boff[c] + p -
+//    p0 - nint[c]] with tag s+1; halo readers poll exactly those entries (halo_pub).
+//  * each CTA publishes its sweep max |delta| as an LL pair; CTA 0's master warp reduces them
+//    in sweep order, applies max|delta| <= eps*mean_cost (dual.cpp:235) and publishes one
+//    control word {stop:32 | verdicts:32}. A CTA starts sweep s only once verdict s-8 exists, so
+//    the result of the stopping sweep k (glam[(k+1)%8]) is never overwritten; sweeps after k are
+//    speculation and are discarded.
+constexpr int kLLRing = 4;
+
+__device__ __forceinline__ void st_ll(unsigned long long* p, double v, unsigned tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long hi = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(hi | (b & 0xffffffffull)),
+               "l"(hi | (b >> 32))
+               : "memory");
+}
+__device__ __forceinline__ void ld_ll_raw(const unsigned long long* p, unsigned long long& w0,
+                                          unsigned long long& w1) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
+__device__ __forceinline__ bool ll_ok(unsigned long long w0, unsigned long long w1, unsigned tag) {
+  return (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag;
+}
+__device__ __forceinline__ double ll_val(unsigned long long w0, unsigned long long w1) {
+  return __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct Sweep4Ctl {  // device-side control block (zeroed before each launch)
+  unsigned long long word;  // {stop (k+1, 0 = running):32 | verdicts published:32}
+  int abort;
+  int sweeps;
+  int converged;
+  int out_buffer;
+  double final_max;
+};
+
+struct Sweep4Args {
+  int n;
+  const int64_t* __restrict__ sptr;
+  const int32_t* __restrict__ swidth;
+  const int32_t* __restrict__ cta_lo;
+  const int32_t* __restrict__ cta_int_hi;
+  const int32_t* __restrict__ cta_nint;
+  const int32_t* __restrict__ boff;
+  const uint16_t* __restrict__ slidx;
+  const double* __restrict__ scost;
+  const int32_t* __restrict__ halo_off;
+  const int32_t* __restrict__ halo;
+  const int32_t* __restrict__ halo_pub;
+  double* glam[8];           // full multipliers: sweep s writes glam[(s+1)%8]
+  unsigned long long* ll;    // [kLLRing][nb][2]
+  int nb;
+  unsigned long long* cmax;  // [kCmaxRing][G][2]
+  double eta;
+  int update;
+  double threshold;
+  int max_sweeps;
+  double* record;
+  int lam_stride;
+  unsigned long long* trace;
+  int trace_first, trace_count;
+};
+
+constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
+
+template <int B, bool RES>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep4(Sweep4Args a, Sweep4Ctl* ctl) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[kSweepThreads / 32];
+  __shared__ int s_stop;
+  __shared__ unsigned long long s_word;  // latest control word seen by the sync warp
+  const int c = blockIdx.x, G = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int sync_warp = nwarps - 1, master_warp = nwarps - 2, ncw = nwarps - 2;
+  const int main_threads = (nwarps - 1) * 32;
+  const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
+  const int p0 = s_lo * 32;
+  const int own = max(0, min(s_hi * 32, a.n) - p0);
+  const int nint = a.cta_nint[c];
+  const int bo = a.boff[c] - nint;  // LL index of own local index lp >= nint is bo + lp
+  const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
+  const int64_t slot0 = a.sptr[s_lo];
+  const int nslots = (int)(a.sptr[s_hi] - slot0);
+  double* regA = reinterpret_cast<double*>(smem);
+  double* regB = regA + (RES ? a.lam_stride : 0);
+  int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
+  double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
+  uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
+  const double* __restrict__ gcost = a.scost + slot0;
+  const uint16_t* __restrict__ glid = a.slidx + slot0;
+  for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
+  if (RES) {
+    for (int i = tid; i < nslots; i += blockDim.x) {
+      cst_s[i] = gcost[i];
+      lid_s[i] = glid[i];
+    }
+    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.glam[0][p0 + i];
+  }
+  if (tid == 0) {
+    s_word = 0ull;
+    s_stop = -1;
+  }
+  __syncthreads();
+
+  if (warp == master_warp) {
+    if (c != 0) return;  // only CTA 0 runs the convergence master
+    // ---- verdict on sweep k once every CTA has published its max |delta| for k
+    unsigned stop = 0;
+    double g = INFINITY;
+    int conv = 0;
+    for (int k = 0; k < a.max_sweeps && !stop; ++k) {
+      const unsigned tag = (unsigned)k + 1;
+      const unsigned long long* row = a.cmax + (size_t)(k % kCmaxRing) * G * 2;
+      double x[kMaxCtaBatch];
+      unsigned pend = 0;
+#pragma unroll
+      for (int b = 0; b < kMaxCtaBatch; ++b) {
+        x[b] = 0.0;
+        if (lane + 32 * b < G) pend |= 1u << b;
+      }
+      const uint64_t t0 = globaltimer_ns();
+      int it = 0;
+      while (__any_sync(0xffffffffu, pend != 0)) {
+        unsigned long long w0[kMaxCtaBatch], w1[kMaxCtaBatch];
+#pragma unroll
+        for (int b = 0; b < kMaxCtaBatch; ++b)
+          if (pend & (1u << b)) ld_ll_raw(row + 2 * (lane + 32 * b), w0[b], w1[b]);
+#pragma unroll
+        for (int b = 0; b < kMaxCtaBatch; ++b)
+          if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], tag)) {
+            x[b] = ll_val(w0[b], w1[b]);
+            pend &= ~(1u << b);
+          }
+        if ((++it & 63) == 0) {
+          int quit = 0;
+          if (lane == 0) {
+            quit = ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs;
+            if (quit) atomicExch(&ctl->abort, 1);
+          }
+          if (__shfl_sync(0xffffffffu, quit, 0)) {
+            stop = (unsigned)k;  // abandon: report what was decided so far
+            break;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, pend != 0)) break;
+      double mx = 0.0;
+#pragma unroll
+      for (int b = 0; b < kMaxCtaBatch; ++b) mx = mx < x[b] ? x[b] : mx;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = mx < y ? y : mx;
+      }
+      g = mx;
+      if (g <= a.threshold) {
+        conv = 1;
+        stop = tag;
+      } else if (k == a.max_sweeps - 1) {
+        stop = tag;
+      }
+      if (lane == 0) {
+        if (a.record) a.record[k] = g;
+        st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | tag);
+      }
+    }
+    if (lane == 0) {
+      if (stop == 0) stop = 1;  // aborted before the first verdict
+      st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | stop);
+      ctl->sweeps = (int)stop;
+      ctl->converged = conv;
+      ctl->final_max = g;
+      ctl->out_buffer = (int)(stop & 7);
+    }
+    return;
+  }
+
+  // ---- main loop: ncw compute warps + the sync warp
+  for (int s = 0;; ++s) {
+    if (warp == 0 && lane == 0) {
+      // sweep s overwrites glam[(s+1)%8]: verdict s-8 must be in (or the solve must have stopped)
+      unsigned long long w = *(volatile unsigned long long*)&s_word;
+      const uint64_t t0 = globaltimer_ns();
+      int it = 0;
+      for (;;) {
+        const unsigned stop = (unsigned)(w >> 32), done = (unsigned)w;
+        if (stop) break;
+        if (s < a.max_sweeps && (int)done >= s - kLamBufs + 1) break;
+        if ((++it & 63) == 0 && (ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs)) {
+          atomicExch(&ctl->abort, 1);
+          w = (unsigned long long)(unsigned)max(s, 1) << 32;
+          break;
+        }
+        w = ld_relaxed_u64(&ctl->word);
+      }
+      s_stop = (w >> 32) ? (int)(w >> 32) - 1 : -1;
+    }
+    named_sync(2, main_threads);  // [A]
+    if (s_stop >= 0) break;
+    if (tid == 0) F2M_TRACE(s, 0);
+    double* lam = (RES && (s & 1)) ? regB : regA;
+    double* lam_next = (s & 1) ? regA : regB;
+    const double* gin = a.glam[s & 7];
+    double* gout = a.glam[(s + 1) & 7];
+    if (!RES) {
+      for (int i = tid; i < own; i += main_threads) lam[i] = __ldcg(gin + p0 + i);
+      named_sync(2, main_threads);
+    }
+    double mx = 0.0;
+    if (warp == sync_warp) {
+      // ---- stage the halo of sweep s: LL entries with tag s (sweep 0: the initial multipliers)
+      const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
+      const uint64_t t0 = globaltimer_ns();
+      for (int base = 0; base < nh; base += 32 * 8) {
+        unsigned pend = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (base + lane + 32 * b < nh) pend |= 1u << b;
+        if (s == 0) {
+          double v[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (pend & (1u << b)) v[b] = __ldcg(gin + a.halo[h0 + base + lane + 32 * b]);
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (pend & (1u << b)) lam[own + base + lane + 32 * b] = v[b];
+          continue;
+        }
+        int it = 0;
+        while (__any_sync(0xffffffffu, pend != 0)) {
+          unsigned long long w0[8], w1[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (pend & (1u << b)) ld_ll_raw(llin + 2 * halo_s[base + lane + 32 * b], w0[b], w1[b]);
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], (unsigned)s)) {
+              lam[own + base + lane + 32 * b] = ll_val(w0[b], w1[b]);
+              pend &= ~(1u << b);
+            }
+          if (base == 0 && it == 0 && lane == 0) F2M_TRACE(s, 1);
+          if ((++it & 15) == 0) {
+            // a neighbour that stopped (verdict reached) never publishes again; a stalled one trips
+            // the watchdog. Either way this sweep's output is discarded.
+            int quit = 0;
+            if (lane == 0) {
+              const unsigned long long w = ld_relaxed_u64(&ctl->word);
+              s_word = w;
+              quit = (w >> 32) != 0 || ld_relaxed(&ctl->abort);
+              if (!quit && globaltimer_ns() - t0 > kWatchdogNs) {
+                atomicExch(&ctl->abort, 1);
+                quit = 1;
+              }
+            }
+            if (__shfl_sync(0xffffffffu, quit, 0)) {
+              pend = 0;
+              base = nh;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) F2M_TRACE(s, 2);
+      named_arrive(1, main_threads);
+      if (lane == 0) s_word = ld_relaxed_u64(&ctl->word);  // off the critical path: for [A]
+    } else {
+      bool halo_ready = false;
+      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
+      for (int sl = s_lo + warp; sl < s_hi; sl += ncw) {
+        if (!halo_ready && sl >= s_int) {
+          named_sync(1, main_threads);
+          halo_ready = true;
+          if (lane == 0) F2M_TRACE(s, 3);
+        }
+        const int p = sl * 32 + lane;
+        if (p >= a.n) continue;
+        const int lp = p - p0;
+        const int lb = (int)(a.sptr[sl] - slot0) + lane;
+        const int w = a.swidth[sl];
+        const double lv = lam[lp];
+        double sv[B + 1];
+#pragma unroll
+        for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
+        int j = 0;
+        for (; j + 8 <= w; j += 8) {
+          int li[8];
+          double cs[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = lb + 32 * (j + u);
+            li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
+            cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+        }
+        for (; j < w; ++j) {
+          const int idx = lb + 32 * j;
+          const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
+          const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
+          topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
+        }
+        const double d = delta_of<B>(sv, a.update);
+        const double nl = dadd(lv, dmul(a.eta, d));
+        if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);  // boundary: publish first
+        if (a.trace && halo_ready && lane == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count)
+          atomicMax(a.trace + ((((size_t)(s - a.trace_first) * gridDim.x + blockIdx.x) << 3) + 7), globaltimer_ns());
+        gout[p] = nl;
+        if (RES) lam_next[lp] = nl;
+        const double ad = fabs(d);
+        mx = mx < ad ? ad : mx;
+      }
+      if (warp == 0 && lane == 0) F2M_TRACE(s, 4);
+      if (!halo_ready) named_sync(1, main_threads);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, mx, off);
+      mx = mx < o ? o : mx;
+    }
+    if (lane == 0) red[warp] = mx;
+    named_sync(2, main_threads);  // [B]
+    if (tid == 0) F2M_TRACE(s, 5);
+    if (warp == 0) {
+      double bm = (lane < nwarps && lane != master_warp) ? red[lane] : 0.0;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, bm, off);
+        bm = bm < o ? o : bm;
+      }
+      if (lane == 0) {
+        st_ll(a.cmax + ((size_t)(s % kCmaxRing) * G + c) * 2, bm, (unsigned)s + 1);
+        F2M_TRACE(s, 6);
+      }
+    }
+  }
+}
+
+template <int B, bool RES>
+static void launch_sweep4(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
+  auto fn = k_gdp_sweep4<B, RES>;
+  F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&a, (void*)&ctl};
+  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kSweepThreads), args, smem, s));
+}
+
+template <bool RES>
+static void dispatch_sweep4(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
+  switch (b) {
+    case 1: launch_sweep4<1, RES>(a, ctl, ctas, smem, s); break;
+    case 2: launch_sweep4<2, RES>(a, ctl, ctas, smem, s); break;
+    case 3: launch_sweep4<3, RES>(a, ctl, ctas, smem, s); break;
+    case 4: launch_sweep4<4, RES>(a, ctl, ctas, smem, s); break;
+    case 5: launch_sweep4<5, RES>(a, ctl, ctas, smem, s); break;
+    case 6: launch_sweep4<6, RES>(a, ctl, ctas, smem, s); break;
+    case 7: launch_sweep4<7, RES>(a, ctl, ctas, smem, s); break;
+    default: launch_sweep4<8, RES>(a, ctl, ctas, smem, s); break;
+  }
+}
+
+// ---------------------------------------------------------------- persistent Jacobi sweep v5
+// v4's LL exchange with the per-sweep critical path shortened:
+//  * two sync warps run up to one sweep AHEAD of the compute warps: the halo of sweep s+1 is
+//    polled and staged into the idle shared-memory region while sweep s is still computing, and
+//    handed over through an mbarrier (no named barrier between the roles);
+//  * boundary rows (the only rows on the inter-CTA critical path) are computed by groups of L
+//    lanes (L = 1..8, as many as the CTA's boundary count allows) that split the row and merge
+//    their partial top-(B+1) lists with a bitonic merge, instead of one thread per row;
+//  * one CTA barrier per sweep: the stop decision for sweep s+1 is taken before barrier B of s.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// keep the B+1 smallest of two ascending lists (bitonic half-cleaner + sort of B+1 elements)
+template <int B>
+__device__ __forceinline__ void topk_merge(double (&s)[B + 1], const double (&o)[B + 1]) {
+#pragma unroll
+  for (int i = 0; i <= B; ++i) s[i] = o[B - i] < s[i] ? o[B - i] : s[i];
+#pragma unroll
+  for (int i = 0; i < B + 1; ++i) {
+#pragma unroll
+    for (int j = 0; j + 1 < B + 1 - i; ++j) {
+      const bool sw = s[j + 1] < s[j];
+      const double lo = sw ? s[j + 1] : s[j];
+      s[j + 1] = sw ? s[j] : s[j + 1];
+      s[j] = lo;
+    }
+  }
+}
+
+constexpr unsigned kPollBackoffNs = 64;
+
+template <int B, bool RES>
+__global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[2][kSweepThreads / 32];
+  __shared__ int s_stop[2];
+  __shared__ volatile int s_done;  // sweeps completed by the compute warps
+  __shared__ volatile int s_exit;
+  __shared__ unsigned long long s_word;
+  __shared__ __align__(8) uint64_t halo_full[2];
+  const int c = blockIdx.x, G = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int master_warp = nwarps - 1, sync0 = nwarps - 3, ncw = nwarps - 3;
+  const int cthreads = ncw * 32;
+  const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
+  const int p0 = s_lo * 32;
+  const int own = max(0, min(s_hi * 32, a.n) - p0);
+  const int nint = a.cta_nint[c];
+  const int bo = a.boff[c] - nint;
+  const int bstart = min((s_int - s_lo) * 32, own);  // boundary phase: local [bstart, own)
+  const int nbnd = own - bstart;
+  int L = 1;
+  while (L < 8 && nbnd * (2 * L) <= cthreads) L *= 2;
+  const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
+  const int64_t slot0 = a.sptr[s_lo];
+  const int nslots = (int)(a.sptr[s_hi] - slot0);
+  double* regA = reinterpret_cast<double*>(smem);
+  double* regB = regA + (RES ? a.lam_stride : 0);
+  int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
+  double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
+  uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
+  const double* __restrict__ gcost = a.scost + slot0;
+  const uint16_t* __restrict__ glid = a.slidx + slot0;
+  for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
+  if (RES) {
+    for (int i = tid; i < nslots; i += blockDim.x) {
+      cst_s[i] = gcost[i];
+      lid_s[i] = glid[i];
+    }
+    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.glam[0][p0 + i];
+  }
+  if (tid == 0) {
+    s_word = 0ull;
+    s_stop[0] = s_stop[1] = -1;
+    s_done = 0;
+    s_exit = 0;
+    mbar_init(&halo_full[0], 64);  // both sync warps, every lane
+    mbar_init(&halo_full[1], 64);
+  }
+  __syncthreads();
+
+  if (warp == master_warp) {
+    if (c != 0) return;
+    unsigned stop = 0;
+    double g = INFINITY;
+    int conv = 0;
+    for (int k = 0; k < a.max_sweeps && !stop; ++k) {
+      const unsigned tag = (unsigned)k + 1;
+      const unsigned long long* row = a.cmax + (size_t)(k % kCmaxRing) * G * 2;
+      double x[kMaxCtaBatch];
+      unsigned pend = 0;
+#pragma unroll
+      for (int b = 0; b < kMaxCtaBatch; ++b) {
+        x[b] = 0.0;
+        if (lane + 32 * b < G) pend |= 1u << b;
+      }
+      const uint64_t t0 = globaltimer_ns();
+      int it = 0;
+      while (__any_sync(0xffffffffu, pend != 0)) {
+        unsigned long long w0[kMaxCtaBatch], w1[kMaxCtaBatch];
+#pragma unroll
+        for (int b = 0; b < kMaxCtaBatch; ++b)
+          if (pend & (1u << b)) ld_ll_raw(row + 2 * (lane + 32 * b), w0[b], w1[b]);
+#pragma unroll
+        for (int b = 0; b < kMaxCtaBatch; ++b)
+          if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], tag)) {
+            x[b] = ll_val(w0[b], w1[b]);
+            pend &= ~(1u << b);
+          }
+        if ((++it & 63) == 0) {
+          int quit = 0;
+          if (lane == 0) {
+            quit = ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs;
+            if (quit) atomicExch(&ctl->abort, 1);
+          }
+          if (__shfl_sync(0xffffffffu, quit, 0)) {
+            stop = (unsigned)k;
+            break;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, pend != 0)) break;
+      double mx = 0.0;
+#pragma unroll
+      for (int b = 0; b < kMaxCtaBatch; ++b) mx = mx < x[b] ? x[b] : mx;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = mx < y ? y : mx;
+      }
+      g = mx;
+      if (g <= a.threshold) {
+        conv = 1;
+        stop = tag;
+      } else if (k == a.max_sweeps - 1) {
+        stop = tag;
+      }
+      if (lane == 0) {
+        if (a.record) a.record[k] = g;
+        st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | tag);
+      }
+    }
+    if (lane == 0) {
+      if (stop == 0) stop = 1;
+      st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | stop);
+      ctl->sweeps = (int)stop;
+      ctl->converged = conv;
+      ctl->final_max = g;
+      ctl->out_buffer = (int)(stop & 7);
+    }
+    return;
+  }
+
+  if (warp >= sync0) {
+    // ---- sync warps: stage the halo of sweep s (LL tag s; sweep 0: the initial multipliers)
+    const int sw = warp - sync0;
+    for (int s = 0;; ++s) {
+      const int need = RES ? s - 1 : s;  // the region being filled is no longer read
+      while (s_done < need && !s_exit) __nanosleep(32);
+      if (s_exit) break;
+      double* lam = (RES && (s & 1)) ? regB : regA;
+      const double* gin = a.glam[s & 7];
+      const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
+      const uint64_t t0 = globaltimer_ns();
+      bool quit = false;
+      for (int base = sw * 32; base < nh && !quit; base += 64 * 8) {
+        unsigned pend = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (base + lane + 64 * b < nh) pend |= 1u << b;
+        if (s == 0) {
+          double v[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (pend & (1u << b)) v[b] = __ldcg(gin + a.halo[h0 + base + lane + 64 * b]);
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (pend & (1u << b)) lam[own + base + lane + 64 * b] = v[b];
+          continue;
+        }
+        int it = 0;
+        while (__any_sync(0xffffffffu, pend != 0)) {
+          const unsigned pend_before = pend;
+          unsigned long long w0[8], w1[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (pend & (1u << b)) ld_ll_raw(llin + 2 * halo_s[base + lane + 64 * b], w0[b], w1[b]);
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], (unsigned)s)) {
+              lam[own + base + lane + 64 * b] = ll_val(w0[b], w1[b]);
+              pend &= ~(1u << b);
+            }
+          if (sw == 0 && base == 0 && it == 0 && lane == 0) F2M_TRACE(s, 1);
+          // back off while nothing arrives: a spinning poller floods the SM's memory pipe that
+          // the compute warps' shared-memory loads share
+          if (__all_sync(0xffffffffu, pend == pend_before)) __nanosleep(kPollBackoffNs);
+          if ((++it & 15) == 0) {
+            int q = 0;
+            if (lane == 0) {
+              const unsigned long long w = ld_relaxed_u64(&ctl->word);
+              s_word = w;
+              q = (w >> 32) != 0 || ld_relaxed(&ctl->abort) || s_exit;
+              if (!q && globaltimer_ns() - t0 > kWatchdogNs) {
+                atomicExch(&ctl->abort, 1);
+                q = 1;
+              }
+            }
+            if (__shfl_sync(0xffffffffu, q, 0)) {
+              pend = 0;
+              quit = true;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (sw == 0 && lane == 0) F2M_TRACE(s, 2);
+      mbar_arrive(&halo_full[RES ? (s & 1) : 0]);
+      if (sw == 0 && lane == 0) s_word = ld_relaxed_u64(&ctl->word);
+    }
+    return;
+  }
+
+  // ---- compute warps
+  for (int s = 0;; ++s) {
+    if (tid == 0) F2M_TRACE(s, 0);
+    double* lam = (RES && (s & 1)) ? regB : regA;
+    double* lam_next = (s & 1) ? regA : regB;
+    const double* gin = a.glam[s & 7];
+    double* gout = a.glam[(s + 1) & 7];
+    if (!RES) {
+      for (int i = tid; i < own; i += cthreads) lam[i] = __ldcg(gin + p0 + i);
+      named_sync(2, cthreads);
+    }
+    double mx = 0.0;
+    // interior slices: one thread per node (throughput-bound phase)
+    for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
+      const int p = sl * 32 + lane;
+      if (p >= a.n) continue;
+      const int lp = p - p0;
+      const int lb = (int)(a.sptr[sl] - slot0) + lane;
+      const int w = a.swidth[sl];
+      const double lv = lam[lp];
+      double sv[B + 1];
+#pragma unroll
+      for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
+      int j = 0;
+      for (; j + 8 <= w; j += 8) {
+        int li[8];
+        double cs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = lb + 32 * (j + u);
+          li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
+          cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+      }
+      for (; j < w; ++j) {
+        const int idx = lb + 32 * j;
+        const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
+        const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
+        topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
+      }
+      const double d = delta_of<B>(sv, a.update);
+      const double nl = dadd(lv, dmul(a.eta, d));
+      gout[p] = nl;
+      if (RES) lam_next[lp] = nl;
+      const double ad = fabs(d);
+      mx = mx < ad ? ad : mx;
+    }
+    if (warp == 0 && lane == 0) F2M_TRACE(s, 4);
+    mbar_wait(&halo_full[RES ? (s & 1) : 0], RES ? ((s >> 1) & 1) : (s & 1));
+    if (warp == 0 && lane == 0) F2M_TRACE(s, 3);
+    // boundary rows: groups of L lanes split each row, then merge (latency-bound phase)
+    {
+      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
+      const int g = tid / L, r = tid - g * L, ng = cthreads / L;
+      for (int base = 0; base < nbnd; base += ng) {
+        const int node = base + g;
+        const bool valid = node < nbnd;
+        double sv[B + 1];
+#pragma unroll
+        for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
+        const int lp = bstart + node;
+        const int p = p0 + lp;
+        double lv = 0.0;
+        if (valid) {
+          const int sl = p >> 5;
+          const int lb = (int)(a.sptr[sl] - slot0) + (p & 31);
+          const int w = a.swidth[sl];
+          lv = lam[lp];
+          for (int j = r; j < w; j += L) {
+            const int idx = lb + 32 * j;
+            const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
+            const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
+            topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
+          }
+        }
+        for (int off = L >> 1; off; off >>= 1) {
+          double o[B + 1];
+#pragma unroll
+          for (int i = 0; i <= B; ++i) o[i] = __shfl_xor_sync(0xffffffffu, sv[i], off);
+          topk_merge<B>(sv, o);
+        }
+        if (valid && r == 0) {
+          const double d = delta_of<B>(sv, a.update);
+          const double nl = dadd(lv, dmul(a.eta, d));
+          if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          gout[p] = nl;
+          if (RES) lam_next[lp] = nl;
+          const double ad = fabs(d);
+          mx = mx < ad ? ad : mx;
+          if (a.trace && s >= a.trace_first && s < a.trace_first + a.trace_count)
+            atomicMax(a.trace + ((((size_t)(s - a.trace_first) * gridDim.x + blockIdx.x) << 3) + 7),
+                      globaltimer_ns());
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, mx, off);
+      mx = mx < o ? o : mx;
+    }
+    if (lane == 0) red[s & 1][warp] = mx;
+    if (warp == 0 && lane == 0) {
+      // stop decision for sweep s+1 (it overwrites glam[(s+2)%8]): verdict s-7 must be in
+      unsigned long long w = s_word;
+      const uint64_t t0 = globaltimer_ns();
+      int it = 0;
+      const int s1 = s + 1;
+      for (;;) {
+        const unsigned stop = (unsigned)(w >> 32), done = (unsigned)w;
+        if (stop) break;
+        if (s1 >= a.max_sweeps) {  // budget spent: stop after this sweep; the master picks k
+          w = (unsigned long long)(unsigned)s1 << 32;
+          break;
+        }
+        if ((int)done >= s1 - kLamBufs + 1) break;
+        if ((++it & 63) == 0 && (ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs)) {
+          atomicExch(&ctl->abort, 1);
+          w = (unsigned long long)(unsigned)s1 << 32;
+          break;
+        }
+        w = ld_relaxed_u64(&ctl->word);
+      }
+      s_word = w;
+      s_stop[s & 1] = (w >> 32) ? (int)(w >> 32) - 1 : -1;
+    }
+    named_sync(2, cthreads);  // [B]
+    if (tid == 0) F2M_TRACE(s, 5);
+    if (warp == 0) {
+      double bm = lane < ncw ? red[s & 1][lane] : 0.0;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, bm, off);
+        bm = bm < o ? o : bm;
+      }
+      if (lane == 0) {
+        st_ll(a.cmax + ((size_t)(s % kCmaxRing) * G + c) * 2, bm, (unsigned)s + 1);
+        s_done = s + 1;
+        F2M_TRACE(s, 6);
+      }
+    }
+    if (s_stop[s & 1] >= 0) break;
+  }
+  if (tid == 0) s_exit = 1;
+}
+
+template <int B, bool RES>
+static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
+  auto fn = k_gdp_sweep5<B, RES>;
+  F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&a, (void*)&ctl};
+  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kSweepThreads), args, smem, s));
+}
+
+template <bool RES>
+static void dispatch_sweep5(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
+  switch (b) {
+    case 1: launch_sweep5<1, RES>(a, ctl, ctas, smem, s); break;
+    case 2: launch_sweep5<2, RES>(a, ctl, ctas, smem, s); break;
+    case 3: launch_sweep5<3, RES>(a, ctl, ctas, smem, s); break;
+    case 4: launch_sweep5<4, RES>(a, ctl, ctas, smem, s); break;
+    case 5: launch_sweep5<5, RES>(a, ctl, ctas, smem, s); break;
+    case 6: launch_sweep5<6, RES>(a, ctl, ctas, smem, s); break;
+    case 7: launch_sweep5<7, RES>(a, ctl, ctas, smem, s); break;
+    default: launch_sweep5<8, RES>(a, ctl, ctas, smem, s); break;
+  }
+}
+
 size_t sweep_smem_limit(int dev) {
   const cudaDeviceProp& p = device_props(dev);
   return p.sharedMemPerBlockOptin > 4096 ? p.sharedMemPerBlockOptin - 4096 : 0;
@@ -595,15 +1380,22 @@ static void launch_sweep(const SweepArgs& a, SweepCtl* ctl, int ctas, cudaStream
                                        args, 0, s));
 }
 
-static int g_force_v1 = -1;  // F2M_SWEEP_V1=1 forces the grid-barrier kernel (A/B testing)
+// F2M_SWEEP_VARIANT=1|3|4|5 picks the sweep kernel for A/B measurements (default 5; 1 whenever the
+// per-CTA local index space does not fit). F2M_SWEEP_V1=1 is the older spelling of variant 1.
+static int g_variant = -1;
 
-static bool use_v1(const Topology& t) {
-  if (g_force_v1 < 0) {
-    const char* e = std::getenv("F2M_SWEEP_V1");
-    g_force_v1 = (e && e[0] == '1') ? 1 : 0;
+static int sweep_variant(const Topology& t) {
+  if (g_variant < 0) {
+    g_variant = 5;
+    if (const char* e = std::getenv("F2M_SWEEP_VARIANT")) g_variant = std::atoi(e);
+    if (const char* e = std::getenv("F2M_SWEEP_V1"))
+      if (e[0] == '1') g_variant = 1;
+    if (g_variant != 1 && g_variant != 3 && g_variant != 4) g_variant = 5;
   }
-  return g_force_v1 == 1 || !t.v2;
+  return t.v2 ? g_variant : 1;
 }
+
+static bool use_v1(const Topology& t) { return sweep_variant(t) == 1; }
 
 SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam0,
                        double* d_lam1, int max_sweeps, double threshold, double* d_record) {
@@ -654,6 +1446,92 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     converged = h.converged;
     final_max = h.final_max;
     outbuf = (h.sweeps & 1) ? 1 : 0;
+  } else if (sweep_variant(t) >= 4) {
+    const int G = t.sweep_ctas;
+    DBuf<double> extra((size_t)6 * std::max(t.n, 1), s);
+    DBuf<Sweep4Ctl> ctl(1, s);
+    const int nb = std::max(t.nboundary, 1);
+    DBuf<unsigned long long> ll((size_t)kLLRing * nb * 2, s);
+    DBuf<unsigned long long> cmax((size_t)kCmaxRing * G * 2, s);
+    // tags restart at 1 every launch: stale words from an earlier launch must not match
+    F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(Sweep4Ctl), s));
+    F2M_CUDA(cudaMemsetAsync(ll.get(), 0, ll.bytes(), s));
+    F2M_CUDA(cudaMemsetAsync(cmax.get(), 0, cmax.bytes(), s));
+    Sweep4Args a;
+    a.n = t.n;
+    a.sptr = t.sptr.get();
+    a.swidth = t.swidth.get();
+    a.cta_lo = t.cta_lo.get();
+    a.cta_int_hi = t.cta_int_hi.get();
+    a.cta_nint = t.cta_nint.get();
+    a.boff = t.boff.get();
+    a.slidx = t.slidx.get();
+    a.scost = g.scost.get();
+    a.halo_off = t.halo_off.get();
+    a.halo = t.halo.get();
+    a.halo_pub = t.halo_pub.get();
+    a.glam[0] = d_lam0;
+    a.glam[1] = d_lam1;
+    for (int i = 2; i < kLamBufs; ++i) a.glam[i] = extra.get() + (size_t)(i - 2) * std::max(t.n, 1);
+    a.ll = ll.get();
+    a.nb = nb;
+    a.cmax = cmax.get();
+    a.eta = cfg.eta;
+    a.update = cfg.update;
+    a.threshold = threshold;
+    a.max_sweeps = max_sweeps;
+    a.record = d_record;
+    a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.trace = nullptr;
+    a.trace_first = a.trace_count = 0;
+    DBuf<unsigned long long> trace;
+    if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {
+      std::sscanf(tr, "%d,%d", &a.trace_first, &a.trace_count);
+      if (a.trace_count > 0) {
+        trace.alloc((size_t)a.trace_count * G * 8, s);
+        F2M_CUDA(cudaMemsetAsync(trace.get(), 0, trace.bytes(), s));
+        a.trace = trace.get();
+      }
+    }
+    F2M_CUDA(cudaEventRecord(e0, s));
+    if (sweep_variant(t) == 5) {
+      if (t.resident) dispatch_sweep5<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+      else dispatch_sweep5<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+      launched("gdp_sweep5");
+    } else {
+      if (t.resident) dispatch_sweep4<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+      else dispatch_sweep4<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+      launched("gdp_sweep4");
+    }
+    F2M_CUDA(cudaEventRecord(e1, s));
+    Sweep4Ctl h;
+    F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    error = h.abort;
+    sweeps = h.sweeps;
+    converged = h.converged;
+    final_max = h.final_max;
+    outbuf = h.out_buffer;
+    if (outbuf >= 2 && t.n > 0)
+      F2M_CUDA(cudaMemcpyAsync(d_lam1, a.glam[outbuf], sizeof(double) * t.n, cudaMemcpyDeviceToDevice, s));
+    if (outbuf >= 2) outbuf = 1;
+    F2M_CUDA(cudaStreamSynchronize(s));
+    if (a.trace) {
+      std::vector<unsigned long long> hbuf(trace.n);
+      F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
+      if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
+        const int hdr[3] = {a.trace_first, a.trace_count, G};
+        std::fwrite(hdr, sizeof(int), 3, f);
+        std::fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
+        std::vector<int32_t> noff(G + 1);
+        F2M_CUDA(cudaMemcpy(noff.data(), t.nbr_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
+        std::vector<int32_t> nbr(std::max(noff[G], 1));
+        F2M_CUDA(cudaMemcpy(nbr.data(), t.nbr.get(), sizeof(int32_t) * nbr.size(), cudaMemcpyDeviceToHost));
+        std::fwrite(noff.data(), sizeof(int32_t), noff.size(), f);
+        std::fwrite(nbr.data(), sizeof(int32_t), noff[G], f);
+        std::fclose(f);
+      }
+    }
   } else {
     const int G = t.sweep_ctas;
     DBuf<double> extra((size_t)6 * std::max(t.n, 1), s);

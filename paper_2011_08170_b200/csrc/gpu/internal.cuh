@@ -145,6 +145,12 @@ struct Topology {
   DBuf<uint16_t> slidx;        // [sell_slots]
   DBuf<int32_t> nbr_off;       // [ctas+1] CTA adjacency (owners of halo nodes)
   DBuf<int32_t> nbr;
+  // v4 sweep (LL halo exchange): CTA c's boundary nodes are positions [p0_c + nint_c, p1_c);
+  // boundary node p publishes its multiplier at LL index boff[c] + (p - p0_c - nint_c).
+  DBuf<int32_t> cta_nint;      // [ctas] interior node count
+  DBuf<int32_t> boff;          // [ctas+1] exclusive prefix of boundary counts
+  DBuf<int32_t> halo_pub;      // [halo entries] LL index of each halo node
+  int nboundary = 0;           // total boundary nodes (LL entries per ring slot)
   int max_local = 0;           // max over CTAs of own + halo
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
