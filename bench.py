@@ -290,7 +290,7 @@ def run_gpu(args):
     if dram is not None and dram_sweeps:
         traffic = dram / dram_sweeps * sw  # per launch of this run's sweep count
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_gdp_sweep<2> (persistent, 148 CTAs x 1024 threads)",
+                "traffic": traffic, "kernel": f2m.last_sweep_kernel_desc(),
                 "algorithmic_bytes_per_sweep": bytes_per_sweep, "sweeps_per_launch": sw,
                 "kernel_ms": kern_ms, "us_per_sweep": 1e3 * kern_ms / sw, "peak_source": peak_src,
                 "share_of_step": (kern_ms * 1e-3) / t_step}

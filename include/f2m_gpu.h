@@ -245,6 +245,9 @@ uint64_t f2m_kernel_launch_count(void);
 /* Device time (ms, CUDA events on the launching stream) of the most recent persistent
  * sweep kernel and the sweeps it ran. */
 int f2m_last_sweep_kernel_ms(double* ms, int* sweeps);
+/* Human-readable description of the most recent sweep kernel launch (variant, template
+ * arguments, grid shape). Valid until the next solve; never NULL. */
+const char* f2m_last_sweep_kernel_desc(void);
 /* Algorithmic bytes per sweep of this graph's GDP kernel:
  * 4(n+1) + 2m*(4+8) + 16n. */
 double f2m_sweep_algorithmic_bytes(const f2m_graph* g);

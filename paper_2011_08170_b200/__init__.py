@@ -52,6 +52,7 @@ from ._f2m import (  # noqa: E402
     jacobi_sweeps,
     kernel_launch_count,
     last_sweep_kernel,
+    last_sweep_kernel_desc,
     load_tsplib,
     make_initial_state,
     node_update_delta,
@@ -76,7 +77,7 @@ __all__ = [
     # B200 extensions
     "DeviceError", "classify_edges", "device_info", "full_solve_arrays", "full_solve_device",
     "full_solve_graph", "gauss_seidel_sweep", "generate_clustered_instance", "graph_from_edges",
-    "jacobi_sweep", "jacobi_sweeps", "kernel_launch_count", "last_sweep_kernel",
+    "jacobi_sweep", "jacobi_sweeps", "kernel_launch_count", "last_sweep_kernel", "last_sweep_kernel_desc",
     "make_initial_state", "set_device", "solve_zero_component", "write_solution",
 ]
 

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <mutex>
 
+#include <vector>
+
 #include "internal.cuh"
 
 namespace f2mgpu {
@@ -39,6 +41,7 @@ Topology::~Topology() {
     sptr.release(); swidth.release(); scol.release(); seid.release(); cta_lo.release();
     halo_off.release(); halo.release(); slidx.release(); nbr_off.release(); nbr.release();
     cta_int_hi.release(); cta_nint.release(); boff.release(); halo_pub.release();
+    sdest.release(); row_nhalo.release();
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
@@ -392,6 +395,30 @@ __global__ void k_slot_lidx(int n, int64_t nslices, const int64_t* __restrict__ 
   }
 }
 
+// halo-last slot order per row (stable within each class) + halo slot count per row
+__global__ void k_halo_last(int n, int64_t nslices, const int64_t* __restrict__ sptr,
+                            const int32_t* __restrict__ swidth, const uint16_t* __restrict__ slidx,
+                            const int32_t* __restrict__ cos, const int32_t* __restrict__ lo,
+                            int32_t* __restrict__ sdest, uint8_t* __restrict__ nhalo) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  int p0, p1;
+  own_range(cos[s], n, lo, p0, p1);
+  const int own = p1 - p0;
+  const int w = swidth[s];
+  const int64_t base = sptr[s] + lane;
+  int nh = 0;
+  for (int j = 0; j < w; ++j) nh += slidx[base + 32 * (int64_t)j] >= own;
+  int io = 0, ih = w - nh;
+  for (int j = 0; j < w; ++j) {
+    const bool h = slidx[base + 32 * (int64_t)j] >= own;
+    sdest[base + 32 * (int64_t)j] = (int32_t)(base + 32 * (int64_t)(h ? ih++ : io++));
+  }
+  const int64_t p = s * 32 + lane;
+  if (p < n) nhalo[p] = (uint8_t)min(nh, 255);
+}
+
 // CTA adjacency: owner of every halo node (halo sorted by (cta, q); owners are monotone in q)
 __global__ void k_nbr_keys(int ctas, const int32_t* __restrict__ hoff, const int32_t* __restrict__ halo,
                            const int32_t* __restrict__ cos, uint64_t* __restrict__ keys) {
@@ -547,6 +574,14 @@ static void build_local_index(Topology& t) {
                                                              t.halo.get(), t.slidx.get());
     launched("slot_lidx");
   }
+  t.sdest.alloc(std::max<int64_t>(slots, 1), s);
+  t.row_nhalo.alloc(std::max(n, 1), s);
+  if (slots > 0) {
+    k_halo_last<<<grid_for(t.nslices * 32, 256), 256, 0, s>>>(n, t.nslices, t.sptr.get(), t.swidth.get(),
+                                                             t.slidx.get(), cos.get(), t.cta_lo.get(),
+                                                             t.sdest.get(), t.row_nhalo.get());
+    launched("halo_last");
+  }
   // CTA adjacency
   t.nbr_off.alloc(G + 1, s);
   {
@@ -599,9 +634,17 @@ static void build_local_index(Topology& t) {
   // [lam regions][halo ids (<= max_local ints)][resident: cost + local index per slot]
   const size_t lam_aligned = (lam_bytes + 15) & ~size_t(15);
   const size_t ids_bytes = (size_t)(lam_aligned / sizeof(double)) * sizeof(int);
-  const size_t resident_bytes =
-      2 * lam_aligned + ids_bytes + (size_t)t.max_cta_slots * (sizeof(double) + sizeof(uint16_t));
-  const size_t streaming_bytes = lam_aligned + ids_bytes;
+  // per-CTA slice table (v5): (slot offset, width) per slice, 16-byte aligned
+  int max_slices = 0;
+  {
+    std::vector<int32_t> lo(G + 1);
+    F2M_CUDA(cudaMemcpy(lo.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
+    for (int c = 0; c < G; ++c) max_slices = std::max(max_slices, lo[c + 1] - lo[c]);
+  }
+  const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int2) + (size_t)max_slices * 32;  // + row halo counts
+  const size_t resident_bytes = 2 * lam_aligned + ids_bytes +
+                                (size_t)t.max_cta_slots * (sizeof(double) + sizeof(uint16_t)) + slice_bytes;
+  const size_t streaming_bytes = lam_aligned + ids_bytes + slice_bytes;
   if (streaming_bytes > limit) return;  // v1 kernel
   // The v3 kernel keeps per-sweep CTA maxima in a ring of 64. A CTA starts sweep s only after
   // its own convergence helper has seen EVERY CTA publish sweep s-7, so no CTA runs more than
@@ -628,7 +671,9 @@ void finalize_topology(Topology& t) {
   // a CTA-local order: interior nodes first, boundary nodes last, each by descending degree
   // (small SELL padding). The partition is fixed before the reorder, which stays inside ranges.
   t.nslices = (n + 31) / 32;
-  t.sweep_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sweep_grid_ctas(t.dev), t.nslices));
+  // one SM stays free for the v5 kernel's convergence-master CTA
+  const int sms = sweep_grid_ctas(t.dev);
+  t.sweep_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms > 1 ? sms - 1 : 1, t.nslices));
   const int G = t.sweep_ctas;
   t.cta_lo.alloc(G + 1, s);
   t.cta_int_hi.alloc(G, s);

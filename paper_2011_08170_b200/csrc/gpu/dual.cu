@@ -21,6 +21,7 @@
 #include <chrono>
 #include <climits>
 #include <cstdlib>
+#include <string>
 
 #include "internal.cuh"
 
@@ -260,6 +261,13 @@ struct Sweep3Args {
   do {                                                                                      \
     if (a.trace && (S) >= a.trace_first && (S) < a.trace_first + a.trace_count)             \
       a.trace[(((size_t)((S) - a.trace_first) * gridDim.x + blockIdx.x) << 3) + (PH)] =      \
+          globaltimer_ns();                                                                 \
+  } while (0)
+
+#define F2M_TRACE16(S, PH)                                                                  \
+  do {                                                                                      \
+    if (a.trace && (S) >= a.trace_first && (S) < a.trace_first + a.trace_count)             \
+      a.trace[(((size_t)((S) - a.trace_first) * (G + 1) + blockIdx.x) << 4) + (PH)] =        \
           globaltimer_ns();                                                                 \
   } while (0)
 
@@ -623,7 +631,8 @@ struct Sweep4Args {
   const int32_t* __restrict__ halo_off;
   const int32_t* __restrict__ halo;
   const int32_t* __restrict__ halo_pub;
-  double* glam[8];           // full multipliers: sweep s writes glam[(s+1)%8]
+  double* gl;                // full multipliers, kLamBufs contiguous buffers: sweep s writes
+  size_t gstride;            // buffer (s+1)%8 at gl + ((s+1)%8)*gstride (no param-space indexing)
   unsigned long long* ll;    // [kLLRing][nb][2]
   int nb;
   unsigned long long* cmax;  // [kCmaxRing][G][2]
@@ -633,6 +642,12 @@ struct Sweep4Args {
   int max_sweeps;
   double* record;
   int lam_stride;
+  const int32_t* __restrict__ sdest;     // v5: slot -> halo-last slot
+  const uint8_t* __restrict__ row_nhalo; // v5: halo slots per row
+  unsigned poll_ns;          // v5: sync-warp back-off between unproductive halo polls
+  int runahead;              // v5: stage the next sweep's halo while this sweep computes
+  int debug;                 // timing experiments only (F2M_SWEEP_DEBUG): 1 = no halo wait
+  int split;                 // v5: scan boundary rows' own-CTA slots before the halo arrives
   unsigned long long* trace;
   int trace_first, trace_count;
 };
@@ -670,7 +685,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep4(Sweep4Args a, S
       cst_s[i] = gcost[i];
       lid_s[i] = glid[i];
     }
-    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.glam[0][p0 + i];
+    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.gl[p0 + i];
   }
   if (tid == 0) {
     s_word = 0ull;
@@ -776,8 +791,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep4(Sweep4Args a, S
     if (tid == 0) F2M_TRACE(s, 0);
     double* lam = (RES && (s & 1)) ? regB : regA;
     double* lam_next = (s & 1) ? regA : regB;
-    const double* gin = a.glam[s & 7];
-    double* gout = a.glam[(s + 1) & 7];
+    const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
+    double* gout = (a.gl + (size_t)((s + 1) & 7) * a.gstride);
     if (!RES) {
       for (int i = tid; i < own; i += main_threads) lam[i] = __ldcg(gin + p0 + i);
       named_sync(2, main_threads);
@@ -963,6 +978,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   } while (!ok);
 }
 
+// warp max of non-negative doubles (|delta|) through their bit patterns (monotone for x >= 0):
+// two REDUX ops instead of five 64-bit shuffle rounds. NaN is skipped like std::max(a, NaN) == a.
+__device__ __forceinline__ unsigned long long warp_max_nonneg(double x) {
+  const unsigned long long v = x == x ? (unsigned long long)__double_as_longlong(x) : 0ull;
+  const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
+}
+
 // keep the B+1 smallest of two ascending lists (bitonic half-cleaner + sort of B+1 elements)
 template <int B>
 __device__ __forceinline__ void topk_merge(double (&s)[B + 1], const double (&o)[B + 1]) {
@@ -982,18 +1007,115 @@ __device__ __forceinline__ void topk_merge(double (&s)[B + 1], const double (&o)
 
 constexpr unsigned kPollBackoffNs = 64;
 
-template <int B, bool RES>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
+// Convergence master: a whole CTA on its own SM. Each round it reads the LL max |delta| of every
+// CTA for a window of kMasterWindow sweeps in one pass (one L2 round trip for all of them), then
+// thread 0 issues the verdicts for the complete sweeps in order (max|delta| <= eps*mean_cost,
+// dual.cpp:235) and publishes {stop:32 | verdicts:32}. A one-sweep-per-round-trip master paces
+// the whole grid at its own latency; the window takes it off the critical path.
+constexpr int kMasterWindow = 16;
+
+__device__ __noinline__ void sweep_master(const unsigned long long* __restrict__ cmax, int max_sweeps,
+                                         double threshold, double* record, unsigned long long* trace,
+                                         int trace_first, int trace_count, Sweep4Ctl* ctl, int G) {
+  __shared__ unsigned long long m_max[kMasterWindow];
+  __shared__ int m_cnt[kMasterWindow];
+  __shared__ int m_base, m_stop, m_quit;
+  __shared__ double m_g;
+  __shared__ int m_conv;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    m_base = 0;
+    m_stop = 0;
+    m_quit = 0;
+    m_g = INFINITY;
+    m_conv = 0;
+  }
+  __syncthreads();
+  const uint64_t t_start = globaltimer_ns();
+  uint64_t t_prog = t_start;
+  for (;;) {
+    const int base = m_base;
+    if (tid < kMasterWindow) {
+      m_max[tid] = 0ull;
+      m_cnt[tid] = 0;
+    }
+    __syncthreads();
+    for (int e = tid; e < kMasterWindow * G; e += blockDim.x) {
+      const int w = e / G, cta = e - w * G, k = base + w;
+      if (k >= max_sweeps) continue;
+      unsigned long long w0, w1;
+      ld_ll_raw(cmax + ((size_t)(k % kCmaxRing) * G + cta) * 2, w0, w1);
+      if (ll_ok(w0, w1, (unsigned)k + 1)) {
+        const double v = ll_val(w0, w1);
+        atomicMax(&m_max[w], v == v ? (unsigned long long)__double_as_longlong(v) : 0ull);
+        atomicAdd(&m_cnt[w], 1);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int k = base;
+      unsigned stop = 0;
+      for (int w = 0; w < kMasterWindow; ++w, ++k) {
+        if (k >= max_sweeps || m_cnt[w] < G) break;
+        const double g = __longlong_as_double((long long)m_max[w]);
+        if (record) record[k] = g;
+        if (trace && k >= trace_first && k < trace_first + trace_count)
+          trace[(((size_t)(k - trace_first) * (G + 1) + G) << 4) + 0] = globaltimer_ns();
+        m_g = g;
+        if (g <= threshold) {
+          m_conv = 1;
+          stop = (unsigned)k + 1;
+          ++k;
+          break;
+        }
+        if (k == max_sweeps - 1) {
+          stop = (unsigned)k + 1;
+          ++k;
+          break;
+        }
+      }
+      const uint64_t now = globaltimer_ns();
+      if (k > base || stop) {
+        st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | (unsigned)k);
+        t_prog = now;
+      } else if (ld_relaxed(&ctl->abort) || now - t_prog > kWatchdogNs) {
+        atomicExch(&ctl->abort, 1);
+        stop = (unsigned)max(base, 1);
+        st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | stop);
+      }
+      m_base = k;
+      m_stop = (int)stop;
+    }
+    __syncthreads();
+    if (m_stop) break;
+    if (m_base == base) __nanosleep(100);  // nothing new yet
+  }
+  if (tid == 0) {
+    ctl->sweeps = m_stop;
+    ctl->converged = m_conv;
+    ctl->final_max = m_g;
+    ctl->out_buffer = m_stop & 7;
+  }
+}
+
+template <int B, bool RES, int NT>
+__global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[2][kSweepThreads / 32];
+  __shared__ double red[2][NT / 32];
   __shared__ int s_stop[2];
   __shared__ volatile int s_done;  // sweeps completed by the compute warps
   __shared__ volatile int s_exit;
+  __shared__ volatile int s_dummy;
+  __shared__ volatile int s_staged[2];
   __shared__ unsigned long long s_word;
-  __shared__ __align__(8) uint64_t halo_full[2];
-  const int c = blockIdx.x, G = gridDim.x;
+  // CTAs 0..G-1 own the partition; CTA G (alone on its SM) is the convergence master
+  const int c = blockIdx.x, G = gridDim.x - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int master_warp = nwarps - 1, sync0 = nwarps - 3, ncw = nwarps - 3;
+  const int sync0 = nwarps - 2, ncw = nwarps - 2;
+  if (c == G) {
+    sweep_master(a.cmax, a.max_sweeps, a.threshold, a.record, a.trace, a.trace_first, a.trace_count, ctl, G);
+    return;
+  }
   const int cthreads = ncw * 32;
   const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
   const int p0 = s_lo * 32;
@@ -1002,8 +1124,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
   const int bo = a.boff[c] - nint;
   const int bstart = min((s_int - s_lo) * 32, own);  // boundary phase: local [bstart, own)
   const int nbnd = own - bstart;
-  int L = 1;
-  while (L < 8 && nbnd * (2 * L) <= cthreads) L *= 2;
   const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
   const int64_t slot0 = a.sptr[s_lo];
   const int nslots = (int)(a.sptr[s_hi] - slot0);
@@ -1012,110 +1132,44 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
   int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
   double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
   uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
+  // per-slice (slot offset, width) of this CTA: no global loads on the sweep path
+  int2* slc = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(lid_s + (RES ? nslots : 0)) + 15) & ~uintptr_t(15));
+  uint8_t* nh_s = reinterpret_cast<uint8_t*>(slc + (s_hi - s_lo));  // halo slots per boundary row
   const double* __restrict__ gcost = a.scost + slot0;
   const uint16_t* __restrict__ glid = a.slidx + slot0;
   for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
+  for (int i = tid; i < s_hi - s_lo; i += blockDim.x)
+    slc[i] = make_int2((int)(a.sptr[s_lo + i] - slot0), a.swidth[s_lo + i]);
+  for (int i = tid; i < nbnd; i += blockDim.x) nh_s[i] = a.row_nhalo[p0 + bstart + i];
   if (RES) {
-    for (int i = tid; i < nslots; i += blockDim.x) {
-      cst_s[i] = gcost[i];
-      lid_s[i] = glid[i];
+    for (int i = tid; i < nslots; i += blockDim.x) {  // rows stored own-first, halo-last
+      const int d = (int)(a.sdest[slot0 + i] - slot0);
+      cst_s[d] = gcost[i];
+      lid_s[d] = glid[i];
     }
-    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.glam[0][p0 + i];
+    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.gl[p0 + i];
   }
   if (tid == 0) {
     s_word = 0ull;
     s_stop[0] = s_stop[1] = -1;
     s_done = 0;
     s_exit = 0;
-    mbar_init(&halo_full[0], 64);  // both sync warps, every lane
-    mbar_init(&halo_full[1], 64);
+    s_staged[0] = s_staged[1] = -1;
   }
   __syncthreads();
-
-  if (warp == master_warp) {
-    if (c != 0) return;
-    unsigned stop = 0;
-    double g = INFINITY;
-    int conv = 0;
-    for (int k = 0; k < a.max_sweeps && !stop; ++k) {
-      const unsigned tag = (unsigned)k + 1;
-      const unsigned long long* row = a.cmax + (size_t)(k % kCmaxRing) * G * 2;
-      double x[kMaxCtaBatch];
-      unsigned pend = 0;
-#pragma unroll
-      for (int b = 0; b < kMaxCtaBatch; ++b) {
-        x[b] = 0.0;
-        if (lane + 32 * b < G) pend |= 1u << b;
-      }
-      const uint64_t t0 = globaltimer_ns();
-      int it = 0;
-      while (__any_sync(0xffffffffu, pend != 0)) {
-        unsigned long long w0[kMaxCtaBatch], w1[kMaxCtaBatch];
-#pragma unroll
-        for (int b = 0; b < kMaxCtaBatch; ++b)
-          if (pend & (1u << b)) ld_ll_raw(row + 2 * (lane + 32 * b), w0[b], w1[b]);
-#pragma unroll
-        for (int b = 0; b < kMaxCtaBatch; ++b)
-          if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], tag)) {
-            x[b] = ll_val(w0[b], w1[b]);
-            pend &= ~(1u << b);
-          }
-        if ((++it & 63) == 0) {
-          int quit = 0;
-          if (lane == 0) {
-            quit = ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs;
-            if (quit) atomicExch(&ctl->abort, 1);
-          }
-          if (__shfl_sync(0xffffffffu, quit, 0)) {
-            stop = (unsigned)k;
-            break;
-          }
-        }
-      }
-      if (__any_sync(0xffffffffu, pend != 0)) break;
-      double mx = 0.0;
-#pragma unroll
-      for (int b = 0; b < kMaxCtaBatch; ++b) mx = mx < x[b] ? x[b] : mx;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double y = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = mx < y ? y : mx;
-      }
-      g = mx;
-      if (g <= a.threshold) {
-        conv = 1;
-        stop = tag;
-      } else if (k == a.max_sweeps - 1) {
-        stop = tag;
-      }
-      if (lane == 0) {
-        if (a.record) a.record[k] = g;
-        st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | tag);
-      }
-    }
-    if (lane == 0) {
-      if (stop == 0) stop = 1;
-      st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | stop);
-      ctl->sweeps = (int)stop;
-      ctl->converged = conv;
-      ctl->final_max = g;
-      ctl->out_buffer = (int)(stop & 7);
-    }
-    return;
-  }
 
   if (warp >= sync0) {
     // ---- sync warps: stage the halo of sweep s (LL tag s; sweep 0: the initial multipliers)
     const int sw = warp - sync0;
     for (int s = 0;; ++s) {
-      const int need = RES ? s - 1 : s;  // the region being filled is no longer read
+      const int need = (RES && a.runahead) ? s - 1 : s;  // the region being filled is no longer read
       while (s_done < need && !s_exit) __nanosleep(32);
       if (s_exit) break;
       double* lam = (RES && (s & 1)) ? regB : regA;
-      const double* gin = a.glam[s & 7];
+      const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
       const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
       const uint64_t t0 = globaltimer_ns();
-      bool quit = false;
+      bool quit = a.debug == 1 && s > 0;  // timing experiment: do not wait for the halo (WRONG results)
       for (int base = sw * 32; base < nh && !quit; base += 64 * 8) {
         unsigned pend = 0;
 #pragma unroll
@@ -1144,10 +1198,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
               lam[own + base + lane + 64 * b] = ll_val(w0[b], w1[b]);
               pend &= ~(1u << b);
             }
-          if (sw == 0 && base == 0 && it == 0 && lane == 0) F2M_TRACE(s, 1);
+          if (sw == 0 && base == 0 && it == 0 && lane == 0) F2M_TRACE16(s, 1);
           // back off while nothing arrives: a spinning poller floods the SM's memory pipe that
           // the compute warps' shared-memory loads share
-          if (__all_sync(0xffffffffu, pend == pend_before)) __nanosleep(kPollBackoffNs);
+          if (__all_sync(0xffffffffu, pend == pend_before) && a.poll_ns) __nanosleep(a.poll_ns);
           if ((++it & 15) == 0) {
             int q = 0;
             if (lane == 0) {
@@ -1167,8 +1221,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
         }
       }
       __syncwarp();
-      if (sw == 0 && lane == 0) F2M_TRACE(s, 2);
-      mbar_arrive(&halo_full[RES ? (s & 1) : 0]);
+      if (sw == 0 && lane == 0) F2M_TRACE16(s, 2);
+      if (lane == 0) s_staged[sw] = s;
+      // hand-off on a hardware barrier (compute warps sleep in bar.sync, no spinning); two ids
+      // alternate so the run-ahead arrival for s+1 can never be counted towards sweep s
+      named_arrive(3 + (s & 1), cthreads + 64);
       if (sw == 0 && lane == 0) s_word = ld_relaxed_u64(&ctl->word);
     }
     return;
@@ -1176,11 +1233,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
 
   // ---- compute warps
   for (int s = 0;; ++s) {
-    if (tid == 0) F2M_TRACE(s, 0);
+    if (tid == 0) F2M_TRACE16(s, 0);
     double* lam = (RES && (s & 1)) ? regB : regA;
     double* lam_next = (s & 1) ? regA : regB;
-    const double* gin = a.glam[s & 7];
-    double* gout = a.glam[(s + 1) & 7];
+    const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
+    double* gout = (a.gl + (size_t)((s + 1) & 7) * a.gstride);
     if (!RES) {
       for (int i = tid; i < own; i += cthreads) lam[i] = __ldcg(gin + p0 + i);
       named_sync(2, cthreads);
@@ -1191,8 +1248,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
       const int p = sl * 32 + lane;
       if (p >= a.n) continue;
       const int lp = p - p0;
-      const int lb = (int)(a.sptr[sl] - slot0) + lane;
-      const int w = a.swidth[sl];
+      const int2 sw2 = slc[sl - s_lo];
+      const int lb = sw2.x + lane;
+      const int w = sw2.y;
       const double lv = lam[lp];
       double sv[B + 1];
 #pragma unroll
@@ -1223,60 +1281,119 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
       const double ad = fabs(d);
       mx = mx < ad ? ad : mx;
     }
-    if (warp == 0 && lane == 0) F2M_TRACE(s, 4);
-    mbar_wait(&halo_full[RES ? (s & 1) : 0], RES ? ((s >> 1) & 1) : (s & 1));
-    if (warp == 0 && lane == 0) F2M_TRACE(s, 3);
-    // boundary rows: groups of L lanes split each row, then merge (latency-bound phase)
-    {
-      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
-      const int g = tid / L, r = tid - g * L, ng = cthreads / L;
-      for (int base = 0; base < nbnd; base += ng) {
-        const int node = base + g;
-        const bool valid = node < nbnd;
-        double sv[B + 1];
+    if (warp == 0 && lane == 0) F2M_TRACE16(s, 4);
+    // boundary rows, first pass (RES): the own-CTA part of the row while the halo is in flight
+    // (slots are stored own-first, halo-last); the top-(B+1) multiset does not depend on order
+    double pv[B + 1];
 #pragma unroll
-        for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-        const int lp = bstart + node;
-        const int p = p0 + lp;
-        double lv = 0.0;
-        if (valid) {
-          const int sl = p >> 5;
-          const int lb = (int)(a.sptr[sl] - slot0) + (p & 31);
-          const int w = a.swidth[sl];
-          lv = lam[lp];
-          for (int j = r; j < w; j += L) {
-            const int idx = lb + 32 * j;
-            const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
-            const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
-            topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
+    for (int i = 0; i <= B; ++i) pv[i] = CUDART_INF;
+    if (RES && a.split && tid < nbnd) {
+      const int lp = bstart + tid, p = p0 + lp;
+      const int2 sw2 = slc[(p >> 5) - s_lo];
+      const int lb = sw2.x + (p & 31);
+      const int jo = sw2.y - nh_s[tid];
+      const double lv = lam[lp];
+      for (int jj = 0; jj < jo; jj += 4) {
+        int li[4];
+        double cs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = jj + u < jo;
+          const int idx = lb + 32 * (ok ? jj + u : 0);
+          li[u] = lid_s[idx];
+          cs[u] = cst_s[idx];
+          if (!ok) {
+            li[u] = lp;
+            cs[u] = CUDART_INF;
           }
         }
-        for (int off = L >> 1; off; off >>= 1) {
-          double o[B + 1];
+        double lu[4];
 #pragma unroll
-          for (int i = 0; i <= B; ++i) o[i] = __shfl_xor_sync(0xffffffffu, sv[i], off);
-          topk_merge<B>(sv, o);
-        }
-        if (valid && r == 0) {
+        for (int u = 0; u < 4; ++u) lu[u] = lam[li[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) topk_bubble<B>(pv, dsub(dsub(cs[u], lv), lu[u]));
+      }
+    }
+    named_sync(3 + (s & 1), cthreads + 64);  // halo of sweep s staged
+    if (warp == 0 && lane == 0) {
+      F2M_TRACE16(s, 3);
+      if (a.trace && s >= a.trace_first && s < a.trace_first + a.trace_count)
+        a.trace[(((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4) + 9] =
+            (unsigned long long)(long long)(min(s_staged[0], s_staged[1]) - s);
+    }
+    long long ck0 = clock64(), ck1 = 0, ck2 = 0, ck3 = 0;
+    // boundary rows, second pass: the halo slots (RES, first batch) or the whole row
+    {
+      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
+      for (int base = 0; base < nbnd; base += cthreads) {
+        if (base + warp * 32 >= nbnd) break;  // warp-uniform: no row for this warp
+        const int node = base + tid;
+        if (node < nbnd) {
+          const int lp = bstart + node, p = p0 + lp;
+          const int2 sw2 = slc[(p >> 5) - s_lo];
+          const int lb = sw2.x + (p & 31);
+          const int w = sw2.y;
+          const bool split = RES && a.split && base == 0;
+          const int j0 = split ? w - nh_s[node] : 0;
+          double sv[B + 1];
+#pragma unroll
+          for (int i = 0; i <= B; ++i) sv[i] = split ? pv[i] : CUDART_INF;
+          const double lv = lam[lp];
+          if (a.trace && tid == 0 && base == 0) {
+            s_dummy = j0 + (int)__double2hiint(lv);
+            ck1 = clock64();
+          }
+          for (int jj = j0; jj < w; jj += 4) {
+            int li[4];
+            double cs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const bool ok = jj + u < w;
+              const int idx = lb + 32 * (ok ? jj + u : j0);
+              li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
+              cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
+              if (!ok) {
+                li[u] = lp;
+                cs[u] = CUDART_INF;
+              }
+            }
+            double lu[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) lu[u] = lam[li[u]];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lu[u]));
+          }
+          if (tid == 0 && base == 0) {
+            s_dummy = (int)__double2hiint(sv[B]);
+            ck2 = clock64();
+            F2M_TRACE16(s, 8);
+          }
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          if (lp >= nint && a.debug != 2) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
           gout[p] = nl;
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
           mx = mx < ad ? ad : mx;
           if (a.trace && s >= a.trace_first && s < a.trace_first + a.trace_count)
-            atomicMax(a.trace + ((((size_t)(s - a.trace_first) * gridDim.x + blockIdx.x) << 3) + 7),
+            atomicMax(a.trace + ((((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4) + 7),
                       globaltimer_ns());
+          if (tid == 0 && base == 0) ck3 = clock64();
         }
       }
     }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      const double o = __shfl_xor_sync(0xffffffffu, mx, off);
-      mx = mx < o ? o : mx;
+    if (a.trace && tid == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count) {
+      unsigned long long* tr = a.trace + (((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4);
+      tr[12] = ck1 - ck0;
+      tr[13] = ck2 - ck1;
+      tr[14] = ck3 - ck2;
+      tr[15] = clock64() - ck0;
     }
-    if (lane == 0) red[s & 1][warp] = mx;
+    {
+      const unsigned long long wm = warp_max_nonneg(mx);
+      if (lane == 0) red[s & 1][warp] = __longlong_as_double((long long)wm);
+    }
+    if (tid == 0) F2M_TRACE16(s, 10);
     if (warp == 0 && lane == 0) {
       // stop decision for sweep s+1 (it overwrites glam[(s+2)%8]): verdict s-7 must be in
       unsigned long long w = s_word;
@@ -1300,20 +1417,16 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
       }
       s_word = w;
       s_stop[s & 1] = (w >> 32) ? (int)(w >> 32) - 1 : -1;
+      F2M_TRACE16(s, 11);
     }
     named_sync(2, cthreads);  // [B]
-    if (tid == 0) F2M_TRACE(s, 5);
-    if (warp == 0) {
-      double bm = lane < ncw ? red[s & 1][lane] : 0.0;
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, bm, off);
-        bm = bm < o ? o : bm;
-      }
+    if (tid == 0) F2M_TRACE16(s, 5);
+    if (warp == ncw - 1) {  // the CTA max goes out from the warp with the least boundary work
+      const unsigned long long bm = warp_max_nonneg(lane < ncw ? red[s & 1][lane] : 0.0);
       if (lane == 0) {
-        st_ll(a.cmax + ((size_t)(s % kCmaxRing) * G + c) * 2, bm, (unsigned)s + 1);
+        st_ll(a.cmax + ((size_t)(s % kCmaxRing) * G + c) * 2, __longlong_as_double((long long)bm), (unsigned)s + 1);
         s_done = s + 1;
-        F2M_TRACE(s, 6);
+        F2M_TRACE16(s, 6);
       }
     }
     if (s_stop[s & 1] >= 0) break;
@@ -1321,25 +1434,28 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep5(Sweep4Args a, S
   if (tid == 0) s_exit = 1;
 }
 
-template <int B, bool RES>
+template <int B, bool RES, int NT>
 static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
-  auto fn = k_gdp_sweep5<B, RES>;
+  auto fn = k_gdp_sweep5<B, RES, NT>;
   F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&a, (void*)&ctl};
-  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kSweepThreads), args, smem, s));
+  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
 }
 
-template <bool RES>
+// Resident (smem) layout: 512 threads per CTA (14 compute warps + 2 sync warps) so that ptxas has
+// 128 registers to keep a row's loads in flight; the streaming layout keeps 1024 threads for
+// memory-level parallelism.
+template <bool RES, int NT>
 static void dispatch_sweep5(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
   switch (b) {
-    case 1: launch_sweep5<1, RES>(a, ctl, ctas, smem, s); break;
-    case 2: launch_sweep5<2, RES>(a, ctl, ctas, smem, s); break;
-    case 3: launch_sweep5<3, RES>(a, ctl, ctas, smem, s); break;
-    case 4: launch_sweep5<4, RES>(a, ctl, ctas, smem, s); break;
-    case 5: launch_sweep5<5, RES>(a, ctl, ctas, smem, s); break;
-    case 6: launch_sweep5<6, RES>(a, ctl, ctas, smem, s); break;
-    case 7: launch_sweep5<7, RES>(a, ctl, ctas, smem, s); break;
-    default: launch_sweep5<8, RES>(a, ctl, ctas, smem, s); break;
+    case 1: launch_sweep5<1, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 2: launch_sweep5<2, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 3: launch_sweep5<3, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 4: launch_sweep5<4, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 5: launch_sweep5<5, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 6: launch_sweep5<6, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 7: launch_sweep5<7, RES, NT>(a, ctl, ctas, smem, s); break;
+    default: launch_sweep5<8, RES, NT>(a, ctl, ctas, smem, s); break;
   }
 }
 
@@ -1371,6 +1487,7 @@ static void dispatch_sweep2(int b, const Sweep3Args& a, SweepCtl2* ctl, int ctas
 }
 
 static double g_last_sweep_ms = 0.0;
+static std::string g_last_sweep_desc = "none";
 static int g_last_sweep_count = 0;
 
 template <int B>
@@ -1425,6 +1542,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.threshold = threshold;
     a.max_sweeps = max_sweeps;
     a.record = d_record;
+    g_last_sweep_desc = "k_gdp_sweep<b=" + std::to_string(cfg.b) + "> (grid barrier, " + std::to_string(t.sweep_ctas) + " CTAs)";
     F2M_CUDA(cudaEventRecord(e0, s));
     switch (cfg.b) {
       case 1: launch_sweep<1>(a, ctl.get(), t.sweep_ctas, s); break;
@@ -1448,7 +1566,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     outbuf = (h.sweeps & 1) ? 1 : 0;
   } else if (sweep_variant(t) >= 4) {
     const int G = t.sweep_ctas;
-    DBuf<double> extra((size_t)6 * std::max(t.n, 1), s);
+    DBuf<double> ring((size_t)kLamBufs * std::max(t.n, 1), s);
     DBuf<Sweep4Ctl> ctl(1, s);
     const int nb = std::max(t.nboundary, 1);
     DBuf<unsigned long long> ll((size_t)kLLRing * nb * 2, s);
@@ -1470,11 +1588,21 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.halo_off = t.halo_off.get();
     a.halo = t.halo.get();
     a.halo_pub = t.halo_pub.get();
-    a.glam[0] = d_lam0;
-    a.glam[1] = d_lam1;
-    for (int i = 2; i < kLamBufs; ++i) a.glam[i] = extra.get() + (size_t)(i - 2) * std::max(t.n, 1);
+    a.gl = ring.get();
+    a.gstride = (size_t)std::max(t.n, 1);
+    if (t.n > 0) F2M_CUDA(cudaMemcpyAsync(ring.get(), d_lam0, sizeof(double) * t.n, cudaMemcpyDeviceToDevice, s));
     a.ll = ll.get();
     a.nb = nb;
+    a.sdest = t.sdest.get();
+    a.row_nhalo = t.row_nhalo.get();
+    a.poll_ns = 64;
+    a.runahead = 1;
+    a.debug = 0;
+    a.split = 1;
+    if (const char* e = std::getenv("F2M_SPLIT")) a.split = std::atoi(e);
+    if (const char* e = std::getenv("F2M_SWEEP_DEBUG")) a.debug = std::atoi(e);
+    if (const char* e = std::getenv("F2M_RUNAHEAD")) a.runahead = std::atoi(e);
+    if (const char* e = std::getenv("F2M_POLL_NS")) a.poll_ns = (unsigned)std::max(0, std::atoi(e));
     a.cmax = cmax.get();
     a.eta = cfg.eta;
     a.update = cfg.update;
@@ -1488,17 +1616,28 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {
       std::sscanf(tr, "%d,%d", &a.trace_first, &a.trace_count);
       if (a.trace_count > 0) {
-        trace.alloc((size_t)a.trace_count * G * 8, s);
+        trace.alloc((size_t)a.trace_count * (G + 1) * 16, s);
         F2M_CUDA(cudaMemsetAsync(trace.get(), 0, trace.bytes(), s));
         a.trace = trace.get();
       }
     }
     F2M_CUDA(cudaEventRecord(e0, s));
-    if (sweep_variant(t) == 5) {
-      if (t.resident) dispatch_sweep5<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
-      else dispatch_sweep5<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
+    if (sweep_variant(t) == 5) {  // + 1 CTA: the convergence master
+      static int nt = -1;
+      if (nt < 0) {
+        const char* e = std::getenv("F2M_SWEEP_NT");
+        nt = (e && std::atoi(e) == 1024) ? 1024 : 512;
+      }
+      g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg.b) + (t.resident ? ", resident, " : ", streaming, ") +
+                          std::to_string(t.resident ? nt : 1024) + "> (persistent: " + std::to_string(G) +
+                          " partition CTAs + 1 convergence-master CTA, LL halo exchange, " +
+                          std::to_string(t.smem_bytes) + " B smem/CTA)";
+      if (t.resident && nt == 512) dispatch_sweep5<true, 512>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+      else if (t.resident) dispatch_sweep5<true, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+      else dispatch_sweep5<false, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       launched("gdp_sweep5");
     } else {
+      g_last_sweep_desc = "k_gdp_sweep4<b=" + std::to_string(cfg.b) + "> (" + std::to_string(G) + " CTAs)";
       if (t.resident) dispatch_sweep4<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
       else dispatch_sweep4<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
       launched("gdp_sweep4");
@@ -1512,16 +1651,18 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     converged = h.converged;
     final_max = h.final_max;
     outbuf = h.out_buffer;
-    if (outbuf >= 2 && t.n > 0)
-      F2M_CUDA(cudaMemcpyAsync(d_lam1, a.glam[outbuf], sizeof(double) * t.n, cudaMemcpyDeviceToDevice, s));
-    if (outbuf >= 2) outbuf = 1;
+    if (t.n > 0)
+      F2M_CUDA(cudaMemcpyAsync(d_lam1, a.gl + (size_t)outbuf * a.gstride, sizeof(double) * t.n,
+                               cudaMemcpyDeviceToDevice, s));
+    outbuf = 1;
     F2M_CUDA(cudaStreamSynchronize(s));
     if (a.trace) {
       std::vector<unsigned long long> hbuf(trace.n);
       F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
       if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
-        const int hdr[3] = {a.trace_first, a.trace_count, G};
-        std::fwrite(hdr, sizeof(int), 3, f);
+        const int hdr[4] = {a.trace_first, a.trace_count, -(sweep_variant(t) == 5 ? G + 1 : G),
+                            sweep_variant(t) == 5 ? 16 : 8};
+        std::fwrite(hdr, sizeof(int), 4, f);
         std::fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
         std::vector<int32_t> noff(G + 1);
         F2M_CUDA(cudaMemcpy(noff.data(), t.nbr_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
@@ -1529,6 +1670,16 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
         F2M_CUDA(cudaMemcpy(nbr.data(), t.nbr.get(), sizeof(int32_t) * nbr.size(), cudaMemcpyDeviceToHost));
         std::fwrite(noff.data(), sizeof(int32_t), noff.size(), f);
         std::fwrite(nbr.data(), sizeof(int32_t), noff[G], f);
+        // per-CTA partition facts: cta_lo[G+1], cta_int_hi[G], cta_nint[G], halo_off[G+1]
+        std::vector<int32_t> tmp(G + 1);
+        F2M_CUDA(cudaMemcpy(tmp.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
+        std::fwrite(tmp.data(), sizeof(int32_t), G + 1, f);
+        F2M_CUDA(cudaMemcpy(tmp.data(), t.cta_int_hi.get(), sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+        std::fwrite(tmp.data(), sizeof(int32_t), G, f);
+        F2M_CUDA(cudaMemcpy(tmp.data(), t.cta_nint.get(), sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+        std::fwrite(tmp.data(), sizeof(int32_t), G, f);
+        F2M_CUDA(cudaMemcpy(tmp.data(), t.halo_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
+        std::fwrite(tmp.data(), sizeof(int32_t), G + 1, f);
         std::fclose(f);
       }
     }
@@ -1575,6 +1726,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       }
     }
     F2M_CUDA(cudaEventRecord(e0, s));
+    g_last_sweep_desc = "k_gdp_sweep3<b=" + std::to_string(cfg.b) + "> (" + std::to_string(G) + " CTAs)";
     if (t.resident) dispatch_sweep2<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
     else dispatch_sweep2<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
     launched("gdp_sweep3");
@@ -2025,6 +2177,8 @@ extern "C" int f2m_solve_duals(const f2m_graph* g, const f2m_engine_config* cfg,
     report->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
+
+extern "C" const char* f2m_last_sweep_kernel_desc(void) { return g_last_sweep_desc.c_str(); }
 
 extern "C" int f2m_last_sweep_kernel_ms(double* ms, int* sweeps) {
   if (ms) *ms = g_last_sweep_ms;

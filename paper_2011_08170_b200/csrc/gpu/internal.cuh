@@ -151,6 +151,11 @@ struct Topology {
   DBuf<int32_t> boff;          // [ctas+1] exclusive prefix of boundary counts
   DBuf<int32_t> halo_pub;      // [halo entries] LL index of each halo node
   int nboundary = 0;           // total boundary nodes (LL entries per ring slot)
+  // v5 split boundary rows: the sweep kernel keeps each row's slots in the order (own-CTA
+  // neighbours, then halo neighbours), so the part of a boundary row that does not depend on
+  // other CTAs is scanned while the halo is still in flight.
+  DBuf<int32_t> sdest;         // [sell_slots] slot index in the halo-last order
+  DBuf<uint8_t> row_nhalo;     // [n] halo slots in the row of each position
   int max_local = 0;           // max over CTAs of own + halo
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel

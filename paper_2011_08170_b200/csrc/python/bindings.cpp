@@ -412,6 +412,7 @@ PYBIND11_MODULE(_f2m, m) {
   });
   m.def("set_device", [](int dev) { f2m::check(f2m_set_device(dev)); }, py::arg("device"));
   m.def("kernel_launch_count", []() { return f2m_kernel_launch_count(); });
+  m.def("last_sweep_kernel_desc", []() { return std::string(f2m_last_sweep_kernel_desc()); });
   m.def("last_sweep_kernel", []() {
     double ms = 0.0;
     int sweeps = 0;

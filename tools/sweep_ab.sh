@@ -1,0 +1,7 @@
+#!/bin/bash
+# A/B of sweep-kernel variants / knobs: us per sweep at 10k / 100k / 200k (2000 sweeps each).
+for cfg in "$@"; do
+  for n in 10000 100000 200000; do
+    echo "$cfg n=$n $(env $cfg timeout 120 python tools/profile_sweep.py $n 2000 2>&1 | grep us/sweep | sed 's/.*us\/sweep=\([0-9.]*\).*/\1/')"
+  done
+done
