@@ -795,7 +795,25 @@ void attach_costs(f2m_graph& g) {
                                                                g.cost.get(), g.scost.get());
     launched("scost");
   }
-  g.mean_cost = sequential_mean(g.cost.get(), t.m, t.stream);
+  g.mean_known = false;
+  g.approx_sum.alloc(1, t.stream);
+  if (t.m > 0) {
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, g.cost.get(), g.approx_sum.get(), t.m, t.stream));
+    DBuf<char> tb(tmp, t.stream);
+    F2M_CUDA(cub::DeviceReduce::Sum(tb.get(), tmp, g.cost.get(), g.approx_sum.get(), t.m, t.stream));
+    launched("approx_cost_sum");
+  } else {
+    F2M_CUDA(cudaMemsetAsync(g.approx_sum.get(), 0, sizeof(double), t.stream));
+  }
+}
+
+double graph_mean(const f2m_graph& g) {
+  if (!g.mean_known) {
+    g.mean_cost = sequential_mean(g.cost.get(), g.topo->m, g.topo->stream);
+    g.mean_known = true;
+  }
+  return g.mean_cost;
 }
 
 void upload_lambda(const f2m_graph& g, const double* h_lambda, double* d_lam_pos) {
@@ -910,7 +928,7 @@ extern "C" int f2m_graph_jittered(const f2m_graph* g, uint64_t seed, int restart
     h->topo = g->topo;
     const Topology& t = *h->topo;
     // cost_scale (solve.cpp:33-35) and amplitude (:40) are host scalars, as in the reference
-    const double scale = g->mean_cost > 0.0 ? g->mean_cost : 1.0;
+    const double scale = graph_mean(*g) > 0.0 ? g->mean_cost : 1.0;
     const double amplitude = perturb_scale * scale;
     const uint64_t state0 = seed * 0x9E3779B97F4A7C15ULL + static_cast<uint64_t>(restart);
     h->cost.alloc(t.m, t.stream);
@@ -935,7 +953,7 @@ extern "C" int f2m_graph_get_info(const f2m_graph* g, f2m_graph_info* out) {
     const Topology& t = *g->topo;
     out->n = t.n;
     out->m = t.m;
-    out->mean_cost = g->mean_cost;
+    out->mean_cost = graph_mean(*g);
     out->min_degree = t.min_deg;
     out->max_degree = t.max_deg;
     out->sell_slots = t.sell_slots;

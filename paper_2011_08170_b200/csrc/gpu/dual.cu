@@ -648,6 +648,13 @@ struct Sweep4Args {
   int runahead;              // v5: stage the next sweep's halo while this sweep computes
   int debug;                 // timing experiments only (F2M_SWEEP_DEBUG): 1 = no halo wait
   int split;                 // v5: scan boundary rows' own-CTA slots before the halo arrives
+  // deferred threshold (v5): defer_eps > 0 -> threshold = defer_eps * mean_cost, where the master
+  // CTA computes mean_cost (sequential sum of cost[0..m) / m, graph.cpp:47-49) during the solve
+  double defer_eps;
+  const double* __restrict__ cost;
+  int64_t m;
+  const double* __restrict__ approx_sum;
+  double* mean_out;
   unsigned long long* trace;
   int trace_first, trace_count;
 };
@@ -1014,15 +1021,39 @@ constexpr unsigned kPollBackoffNs = 64;
 // the whole grid at its own latency; the window takes it off the critical path.
 constexpr int kMasterWindow = 16;
 
+// CTA barrier of the master's verdict threads (all but warp 1 when warp 1 computes the mean)
+__device__ __forceinline__ void master_sync(bool mean_warp_busy) {
+  if (mean_warp_busy) named_sync(5, (int)blockDim.x - 32);
+  else __syncthreads();
+}
+
 __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__ cmax, int max_sweeps,
                                          double threshold, double* record, unsigned long long* trace,
-                                         int trace_first, int trace_count, Sweep4Ctl* ctl, int G) {
+                                         int trace_first, int trace_count, Sweep4Ctl* ctl, int G,
+                                         double defer_eps, const double* __restrict__ cost, int64_t m,
+                                         const double* __restrict__ approx_sum, double* mean_out) {
   __shared__ unsigned long long m_max[kMasterWindow];
   __shared__ int m_cnt[kMasterWindow];
   __shared__ int m_base, m_stop, m_quit;
   __shared__ double m_g;
   __shared__ int m_conv;
+  __shared__ volatile int m_thr_ready;
+  __shared__ double m_thr, m_lo, m_hi;
+  __shared__ double m_tile[2][256];
   const int tid = threadIdx.x;
+  if (tid == 0) {
+    m_thr_ready = defer_eps > 0.0 ? 0 : 1;
+    m_thr = threshold;
+    if (defer_eps > 0.0) {
+      // |sequential sum - any-order sum| <= 2 gamma_{m-1} * sum(c) for c >= 0; the mean's division
+      // and the product with eps add 2u. delta is a generous over-estimate of the relative gap.
+      const double u = 1.1102230246251565e-16;
+      const double delta = 4.0 * ((double)m + 8.0) * u;
+      const double est = m > 0 ? *approx_sum / (double)m : 0.0;
+      m_lo = defer_eps * est * (1.0 - 2.0 * delta);
+      m_hi = defer_eps * est * (1.0 + 2.0 * delta);
+    }
+  }
   if (tid == 0) {
     m_base = 0;
     m_stop = 0;
@@ -1031,6 +1062,36 @@ __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__
     m_conv = 0;
   }
   __syncthreads();
+  if (defer_eps > 0.0 && (tid >> 5) == 1) {
+    // graph.cpp:47-49: mean_cost = (sum over edges in order of cost) / m, one fp64 chain; lanes
+    // stage 256-cost tiles (double-buffered) while lane 0 adds
+    const int lane = tid & 31;
+    double acc = 0.0;
+    const int64_t ntiles = (m + 255) / 256;
+    for (int i = lane; i < 256; i += 32) m_tile[0][i] = i < m ? cost[i] : 0.0;
+    __syncwarp();
+    for (int64_t t = 0; t < ntiles; ++t) {
+      const int cur = t & 1;
+      if (t + 1 < ntiles) {
+        const int64_t b = (t + 1) * 256;
+        for (int i = lane; i < 256; i += 32) m_tile[cur ^ 1][i] = b + i < m ? cost[b + i] : 0.0;
+      }
+      if (lane == 0) {
+        const int cnt = (int)min64(256, m - t * 256);
+        for (int i = 0; i < cnt; ++i) acc = dadd(acc, m_tile[cur][i]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const double mean = m > 0 ? __ddiv_rn(acc, (double)m) : 0.0;
+      *mean_out = mean;
+      m_thr = dmul(defer_eps, mean);  // cfg.eps * mean_cost (dual.cpp:221)
+      __threadfence_block();
+      m_thr_ready = 1;
+    }
+    return;
+  }
+  if (defer_eps > 0.0 && (tid >> 5) == 1) return;
   const uint64_t t_start = globaltimer_ns();
   uint64_t t_prog = t_start;
   for (;;) {
@@ -1039,8 +1100,10 @@ __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__
       m_max[tid] = 0ull;
       m_cnt[tid] = 0;
     }
-    __syncthreads();
-    for (int e = tid; e < kMasterWindow * G; e += blockDim.x) {
+    master_sync(defer_eps > 0.0);
+    const int nthr = defer_eps > 0.0 ? (int)blockDim.x - 32 : (int)blockDim.x;
+    const int rank = (defer_eps > 0.0 && tid >= 64) ? tid - 32 : tid;
+    for (int e = rank; e < kMasterWindow * G; e += nthr) {
       const int w = e / G, cta = e - w * G, k = base + w;
       if (k >= max_sweeps) continue;
       unsigned long long w0, w1;
@@ -1051,18 +1114,28 @@ __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__
         atomicAdd(&m_cnt[w], 1);
       }
     }
-    __syncthreads();
+    master_sync(defer_eps > 0.0);
     if (tid == 0) {
       int k = base;
       unsigned stop = 0;
       for (int w = 0; w < kMasterWindow; ++w, ++k) {
         if (k >= max_sweeps || m_cnt[w] < G) break;
         const double g = __longlong_as_double((long long)m_max[w]);
+        bool below;
+        if (m_thr_ready) {
+          below = g <= m_thr;
+        } else if (g > m_hi) {
+          below = false;  // above any threshold the exact mean can give
+        } else if (g <= m_lo) {
+          below = true;   // below any threshold the exact mean can give
+        } else {
+          break;          // undecidable until the exact mean is in: retry next round
+        }
         if (record) record[k] = g;
         if (trace && k >= trace_first && k < trace_first + trace_count)
           trace[(((size_t)(k - trace_first) * (G + 1) + G) << 4) + 0] = globaltimer_ns();
         m_g = g;
-        if (g <= threshold) {
+        if (below) {
           m_conv = 1;
           stop = (unsigned)k + 1;
           ++k;
@@ -1086,7 +1159,7 @@ __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__
       m_base = k;
       m_stop = (int)stop;
     }
-    __syncthreads();
+    master_sync(defer_eps > 0.0);
     if (m_stop) break;
     if (m_base == base) __nanosleep(100);  // nothing new yet
   }
@@ -1113,7 +1186,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int sync0 = nwarps - 2, ncw = nwarps - 2;
   if (c == G) {
-    sweep_master(a.cmax, a.max_sweeps, a.threshold, a.record, a.trace, a.trace_first, a.trace_count, ctl, G);
+    sweep_master(a.cmax, a.max_sweeps, a.threshold, a.record, a.trace, a.trace_first, a.trace_count, ctl, G,
+                 a.defer_eps, a.cost, a.m, a.approx_sum, a.mean_out);
     return;
   }
   const int cthreads = ncw * 32;
@@ -1461,7 +1535,8 @@ static void dispatch_sweep5(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas
 
 size_t sweep_smem_limit(int dev) {
   const cudaDeviceProp& p = device_props(dev);
-  return p.sharedMemPerBlockOptin > 4096 ? p.sharedMemPerBlockOptin - 4096 : 0;
+  // headroom for the kernels' static shared memory (v5: ~4.5 KB incl. the master's tiles)
+  return p.sharedMemPerBlockOptin > 8192 ? p.sharedMemPerBlockOptin - 8192 : 0;
 }
 
 template <int B, bool RES>
@@ -1515,11 +1590,16 @@ static int sweep_variant(const Topology& t) {
 static bool use_v1(const Topology& t) { return sweep_variant(t) == 1; }
 
 SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam0,
-                       double* d_lam1, int max_sweeps, double threshold, double* d_record) {
+                       double* d_lam1, int max_sweeps, double threshold, double* d_record,
+                       double defer_eps) {
   const Topology& t = *g.topo;
   cudaStream_t s = t.stream;
   SweepResult r;
   if (max_sweeps <= 0) return r;
+  if (defer_eps > 0.0 && (g.mean_known || sweep_variant(t) != 5)) {
+    threshold = defer_eps * graph_mean(g);  // host fp64 product, no FMA: == cfg.eps * mean_cost
+    defer_eps = 0.0;
+  }
   cudaEvent_t e0, e1;
   F2M_CUDA(cudaEventCreate(&e0));
   F2M_CUDA(cudaEventCreate(&e1));
@@ -1597,6 +1677,12 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.row_nhalo = t.row_nhalo.get();
     a.poll_ns = 64;
     a.runahead = 1;
+    DBuf<double> mean_out(1, s);
+    a.defer_eps = defer_eps;
+    a.cost = g.cost.get();
+    a.m = t.m;
+    a.approx_sum = g.approx_sum.get();
+    a.mean_out = mean_out.get();
     a.debug = 0;
     a.split = 1;
     if (const char* e = std::getenv("F2M_SPLIT")) a.split = std::atoi(e);
@@ -1645,7 +1731,13 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     F2M_CUDA(cudaEventRecord(e1, s));
     Sweep4Ctl h;
     F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    double hmean = 0.0;
+    if (defer_eps > 0.0) F2M_CUDA(cudaMemcpyAsync(&hmean, mean_out.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
+    if (defer_eps > 0.0 && !h.abort) {
+      g.mean_cost = hmean;  // bit-identical to sequential_mean (same chain, same order)
+      g.mean_known = true;
+    }
     error = h.abort;
     sweeps = h.sweeps;
     converged = h.converged;
@@ -2028,7 +2120,10 @@ void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const 
   } else {
     initial_state_device(g, cfg, l0.get());
   }
-  const double threshold = cfg.eps * g.mean_cost;  // dual.cpp:221
+  // threshold = eps * mean_cost (dual.cpp:221); with the mean still unknown the v5 kernel
+  // computes it during the solve
+  const bool defer = !g.mean_known && cfg.mode == 0 && cfg.max_sweeps > 0;
+  const double threshold = defer ? 0.0 : cfg.eps * graph_mean(g);
   rep.converged = 0;
   rep.sweeps = 0;
   rep.final_max_abs_delta = INFINITY;
@@ -2036,7 +2131,8 @@ void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const 
   if (cfg.max_sweeps > 0) {
     check_degree(g, cfg.b);
     if (cfg.mode == 0) {
-      SweepResult r = run_jacobi(g, cfg, l0.get(), l1.get(), cfg.max_sweeps, threshold, nullptr);
+      SweepResult r = run_jacobi(g, cfg, l0.get(), l1.get(), cfg.max_sweeps, threshold, nullptr,
+                                 defer ? cfg.eps : 0.0);
       rep.sweeps = r.sweeps;
       rep.converged = r.converged;
       rep.final_max_abs_delta = r.final_max_abs_delta;

@@ -168,7 +168,12 @@ struct f2m_graph {
   std::shared_ptr<f2mgpu::Topology> topo;
   f2mgpu::DBuf<double> cost;   // [m] reference edge order
   f2mgpu::DBuf<double> scost;  // [sell_slots] per SELL slot (+inf on padding)
-  double mean_cost = 0.0;
+  // mean_cost (graph.cpp:47-49, a SEQUENTIAL fp64 sum in edge order) is computed lazily: the
+  // GDP sweep kernel computes it itself, off the critical path, on the first solve (its master
+  // CTA decides early verdicts from a parallel estimate with a rigorous error bound).
+  mutable double mean_cost = 0.0;
+  mutable bool mean_known = false;
+  f2mgpu::DBuf<double> approx_sum;  // [1] parallel sum of the costs (device)
 };
 
 namespace f2mgpu {
@@ -198,6 +203,8 @@ void identity_perm(Topology& t);
 // cost -> scost, mean_cost (bit-exact sequential sum on the device).
 void attach_costs(f2m_graph& g);
 double sequential_mean(const double* d_cost, int64_t m, cudaStream_t s);
+// The graph's mean_cost, computing it (sequential sum on the device) if still unknown.
+double graph_mean(const f2m_graph& g);
 
 // Lambda layout conversion (host orig order <-> device position order).
 void upload_lambda(const f2m_graph& g, const double* h_lambda, double* d_lam_pos);
@@ -212,8 +219,11 @@ struct SweepResult {
   double final_max_abs_delta = INFINITY;
   int out_buffer = 0;  // which of the two buffers holds the result
 };
+// threshold < 0: run exactly max_sweeps. defer_eps > 0 (threshold ignored): the threshold is
+// defer_eps * mean_cost with mean_cost still unknown; the v5 kernel computes it (and g learns it).
 SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam0,
-                       double* d_lam1, int max_sweeps, double threshold, double* d_record);
+                       double* d_lam1, int max_sweeps, double threshold, double* d_record,
+                       double defer_eps = 0.0);
 void validate_engine(const f2m_engine_config& cfg);
 void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const double* d_init,
                         DBuf<double>& d_lam_out, f2m_convergence_report& rep);

@@ -27,7 +27,7 @@ static double effective_tol(const f2m_run_config& rc) {  // solve.cpp:16-18
 }
 
 static double cost_scale(const f2m_graph& g) {  // solve.cpp:33-35
-  return g.mean_cost > 0.0 ? g.mean_cost : 1.0;
+  return graph_mean(g) > 0.0 ? g.mean_cost : 1.0;
 }
 
 static double seconds_since(std::chrono::steady_clock::time_point t0) {
