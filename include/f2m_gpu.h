@@ -239,6 +239,42 @@ int f2m_full_solve_device(int n, const double* d_xy, int rounded, const f2m_run_
                           double* d_x, int64_t d_x_capacity, double* d_lambda,
                           f2m_solve_outcome* out, f2m_graph** graph_out);
 
+/* ---- node-sharded multi-GPU GDP -------------------------------------
+ * One process per GPU, each holding the (replicated) graph. Rank r owns the spatial
+ * positions [r*stride, min(n, (r+1)*stride)), stride = ceil(n / world), so the concatenation
+ * of the ranks' shard buffers in rank order is the full multiplier vector in position order
+ * (padded to world*stride) — exactly what an NCCL all-gather produces. A Jacobi sweep of a
+ * shard reads only that full vector, so the sharded solve is bit-identical to the one-GPU
+ * solve for every world size (dual.cpp:129-167 freezes lambda for the whole sweep).
+ * The collectives themselves (all-gather of the shards, max-all-reduce of |delta|) are
+ * issued by the caller (NCCL through torch.distributed, paper_2011_08170_b200/sharded.py).
+ * All calls below are stream-ordered on the caller's `stream` (a cudaStream_t; NULL = the
+ * legacy default stream) and do not synchronise, so they can be captured in a CUDA graph. */
+typedef struct f2m_shard f2m_shard;
+int f2m_shard_create(const f2m_graph* g, int rank, int world, f2m_shard** out);
+void f2m_shard_destroy(f2m_shard* s);
+typedef struct {
+  int n;          /* nodes of the graph */
+  int rank, world;
+  int begin, end; /* owned positions [begin, end) */
+  int stride;     /* shard buffer length (positions per rank, padded) */
+  int64_t slots;  /* SELL slots of the owned rows */
+} f2m_shard_info;
+int f2m_shard_get_info(const f2m_shard* s, f2m_shard_info* out);
+/* One Jacobi sweep (jacobi_sweep, dual.cpp:129-167) of the owned rows: reads d_lam_full
+ * (world*stride doubles, position order), writes the updated owned multipliers to
+ * d_lam_shard (stride doubles; padding entries are written as 0) and raises *d_max_bits to
+ * the bit pattern of max |delta| over the owned rows (atomic max on the IEEE bits of a
+ * non-negative double; the caller zeroes it). */
+int f2m_shard_sweep(const f2m_shard* s, const f2m_engine_config* cfg, const double* d_lam_full,
+                    double* d_lam_shard, unsigned long long* d_max_bits, void* stream);
+/* Initial multipliers (make_initial_state, dual.cpp:194-208) in POSITION order into
+ * d_lam_pos (n doubles), and position-order <-> node-id-order conversions on the device. */
+int f2m_initial_state_positions(const f2m_graph* g, const f2m_engine_config* cfg, double* d_lam_pos,
+                                void* stream);
+int f2m_positions_to_ids(const f2m_graph* g, const double* d_pos, double* d_ids, void* stream);
+int f2m_ids_to_positions(const f2m_graph* g, const double* d_ids, double* d_pos, void* stream);
+
 /* ---- instrumentation (bench.py / tests) ----------------------------------------------- */
 /* Number of kernels this library launched since load (all entry points). */
 uint64_t f2m_kernel_launch_count(void);

@@ -50,19 +50,6 @@ __device__ __forceinline__ void topk_insert(double (&s)[B + 1], double val) {
   }
 }
 
-// Branch-free variant for the sweep kernels: bubble val through the sorted list. A NaN val
-// compares false everywhere and falls off the end, like the guarded insert above.
-template <int B>
-__device__ __forceinline__ void topk_bubble(double (&s)[B + 1], double val) {
-#pragma unroll
-  for (int i = 0; i < B; ++i) {
-    const bool lt = val < s[i];
-    const double lo = lt ? val : s[i];
-    val = lt ? s[i] : val;
-    s[i] = lo;
-  }
-  s[B] = val < s[B] ? val : s[B];
-}
 
 template <int B>
 __device__ __forceinline__ double delta_of(const double (&s)[B + 1], int update) {

@@ -253,6 +253,22 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+// Keeps the B+1 smallest values of a row in ascending s[0..B] (s starts at +inf): bubble val
+// through the sorted list, branch-free. The kept multiset equals the reference's insertion
+// (smallest_adjusted, dual.cpp:44-58) whatever the visiting order; a NaN val compares false
+// everywhere and falls off the end, as `val < s[b]` rejects it in the reference.
+template <int B>
+__device__ __forceinline__ void topk_bubble(double (&s)[B + 1], double val) {
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const bool lt = val < s[i];
+    const double lo = lt ? val : s[i];
+    val = lt ? s[i] : val;
+    s[i] = lo;
+  }
+  s[B] = val < s[B] ? val : s[B];
+}
+
 __device__ __forceinline__ uint64_t splitmix64_at(uint64_t state0, uint64_t draw_index) {
   // SplitMix64 (instance.hpp:54-60) is counter-based: the state before draw j (0-based) is
   // state0 + j*gamma, and next() first adds gamma.

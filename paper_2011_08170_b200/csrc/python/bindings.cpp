@@ -395,6 +395,75 @@ PYBIND11_MODULE(_f2m, m) {
       py::arg("n"), py::arg("d_xy"), py::arg("rounded"), py::arg("k"), py::arg("eps"), py::arg("max_sweeps"),
       py::arg("d_x"), py::arg("x_capacity"), py::arg("d_lambda"), py::arg("seed") = 0, py::arg("max_restarts") = 5);
 
+  // --- node-sharded multi-GPU GDP; driven by paper_2011_08170_b200/sharded.py.
+  // Device pointers and CUDA streams cross as integers (torch .data_ptr() / .cuda_stream).
+  struct Shard {
+    f2m_shard* h = nullptr;
+    f2m::Graph graph;  // keeps the graph (and its device costs) alive
+    f2m_engine_config cfg{};
+    ~Shard() { f2m_shard_destroy(h); }
+  };
+  py::class_<Shard, std::shared_ptr<Shard>>(m, "Shard")
+      .def("info", [](const Shard& sh) {
+        f2m_shard_info i{};
+        f2m::check(f2m_shard_get_info(sh.h, &i));
+        return py::dict(py::arg("n") = i.n, py::arg("rank") = i.rank, py::arg("world") = i.world,
+                        py::arg("begin") = i.begin, py::arg("end") = i.end, py::arg("stride") = i.stride,
+                        py::arg("slots") = i.slots);
+      })
+      .def("sweep",
+           [](const Shard& sh, std::uintptr_t lam_full, std::uintptr_t lam_shard, std::uintptr_t max_bits,
+              std::uintptr_t stream) {
+             f2m::check(f2m_shard_sweep(sh.h, &sh.cfg, reinterpret_cast<const double*>(lam_full),
+                                        reinterpret_cast<double*>(lam_shard),
+                                        reinterpret_cast<unsigned long long*>(max_bits),
+                                        reinterpret_cast<void*>(stream)));
+           },
+           py::arg("lam_full"), py::arg("lam_shard"), py::arg("max_bits"), py::arg("stream") = 0);
+  m.def(
+      "shard_create",
+      [](const f2m::Graph& graph, int rank, int world, int b, double eta, const std::string& update) {
+        auto sh = std::make_shared<Shard>();
+        sh->graph = graph;
+        sh->cfg.b = b;
+        sh->cfg.eta = eta;
+        sh->cfg.eps = 1e-9;
+        sh->cfg.max_sweeps = 1;
+        sh->cfg.update = update == "paper-difference" ? 1 : 0;
+        f2m::check(f2m_engine_config_validate(&sh->cfg));
+        f2m::check(f2m_shard_create(graph.handle(), rank, world, &sh->h));
+        return sh;
+      },
+      py::arg("graph"), py::arg("rank"), py::arg("world"), py::arg("b") = 2, py::arg("eta") = 0.5,
+      py::arg("update") = "midpoint");
+  m.def(
+      "initial_state_positions",
+      [](const f2m::Graph& graph, std::uintptr_t d_lam_pos, int b, const std::string& init, std::uintptr_t stream) {
+        f2m_engine_config c{};
+        c.b = b;
+        c.eta = 0.5;
+        c.eps = 1e-9;
+        c.init = init == "zero" ? 1 : 0;
+        f2m::check(f2m_initial_state_positions(graph.handle(), &c, reinterpret_cast<double*>(d_lam_pos),
+                                               reinterpret_cast<void*>(stream)));
+      },
+      py::arg("graph"), py::arg("d_lam_pos"), py::arg("b") = 2, py::arg("init") = "local-midpoint",
+      py::arg("stream") = 0);
+  m.def(
+      "positions_to_ids",
+      [](const f2m::Graph& graph, std::uintptr_t d_pos, std::uintptr_t d_ids, std::uintptr_t stream) {
+        f2m::check(f2m_positions_to_ids(graph.handle(), reinterpret_cast<const double*>(d_pos),
+                                        reinterpret_cast<double*>(d_ids), reinterpret_cast<void*>(stream)));
+      },
+      py::arg("graph"), py::arg("d_pos"), py::arg("d_ids"), py::arg("stream") = 0);
+  m.def(
+      "ids_to_positions",
+      [](const f2m::Graph& graph, std::uintptr_t d_ids, std::uintptr_t d_pos, std::uintptr_t stream) {
+        f2m::check(f2m_ids_to_positions(graph.handle(), reinterpret_cast<const double*>(d_ids),
+                                        reinterpret_cast<double*>(d_pos), reinterpret_cast<void*>(stream)));
+      },
+      py::arg("graph"), py::arg("d_ids"), py::arg("d_pos"), py::arg("stream") = 0);
+
   m.def("write_lp", [](const f2m::Graph& graph) {
     std::ostringstream out;
     f2m::write_lp(graph, out);

@@ -1,0 +1,181 @@
+"""Node-sharded multi-GPU GDP: the sharded solve must be bit-identical to the
+single-process solve for every world size.
+
+CPU (world 2, gloo, two processes): the collective schedule of paper_2011_08170_b200/sharded.py
+(run_sharded_jacobi) driven by a numpy restatement of a shard's Jacobi rows, against the C oracle's
+solve_duals (which is pinned to the reference's golden vectors).
+GPU: the CUDA shard kernel + the same schedule with in-process shards (LocalComm, worlds 1..8) and
+through torch.distributed/NCCL (world 1), against the persistent one-GPU solver.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc  # checker only
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _shard_rows(g, begin, end):
+    """Padded incident lists of nodes [begin, end): neighbour ids and costs (+inf padding)."""
+    deg = np.zeros(g.n, np.int64)
+    np.add.at(deg, g.eu, 1)
+    np.add.at(deg, g.ev, 1)
+    rows = end - begin
+    width = int(deg[begin:end].max()) if rows else 1
+    nb = np.repeat(np.arange(begin, end)[:, None], width, axis=1)
+    cost = np.full((rows, width), np.inf)
+    fill = np.zeros(rows, np.int64)
+    for u, v, c in zip(g.eu, g.ev, g.cost):
+        for a, b in ((u, v), (v, u)):
+            if begin <= a < end:
+                r = a - begin
+                nb[r, fill[r]] = b
+                cost[r, fill[r]] = c
+                fill[r] += 1
+    return nb, cost
+
+
+def _numpy_sweep(nb, cost, begin, end, b=2, eta=0.5):
+    """One Jacobi sweep of rows [begin, end) in the reference's arithmetic (dual.cpp:33-68,
+    140-161): values (c - l_v) - l_u, the b-th and (b+1)-th smallest, midpoint update."""
+    def fn(lam_full, out, bits):
+        lam = lam_full.numpy()
+        lv = lam[begin:end]
+        val = (cost - lv[:, None]) - lam[nb]
+        s = np.sort(val, axis=1)
+        d = 0.5 * (s[:, b - 1] + s[:, b])
+        o = out.numpy()
+        o[:] = 0.0
+        o[: end - begin] = lv + eta * d
+        m = np.max(np.abs(d)) if len(d) else 0.0
+        mb = np.array([m], np.float64).view(np.int64)[0]
+        bits.copy_(torch.maximum(bits, torch.tensor(mb, dtype=torch.int64)))
+    return fn
+
+
+def _gloo_worker(rank, world, port, n, seed, eps, max_sweeps, out_path):
+    import torch.distributed as dist
+
+    from paper_2011_08170_b200.sharded import TorchDistComm, run_sharded_jacobi
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = orc.build_knn_graph(orc.generate_instance(n, seed), 10)
+        stride = (g.n + world - 1) // world
+        begin, end = min(g.n, rank * stride), min(g.n, (rank + 1) * stride)
+        nb, cost = _shard_rows(g, begin, end)
+        lam0 = torch.zeros(stride * world, dtype=torch.float64)
+        lam0[: g.n] = torch.from_numpy(orc.initial_state(g))
+        res = run_sharded_jacobi([_numpy_sweep(nb, cost, begin, end)], TorchDistComm(), stride, lam0,
+                                 eps * g.mean_cost(), max_sweeps, chunk=7)
+        if rank == 0:
+            np.savez(out_path, lam=res.lam_full[: g.n].numpy(), sweeps=res.sweeps, conv=res.converged,
+                     fmax=res.final_max_abs_delta, record=np.array(res.record))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("max_sweeps", [20000, 37])
+def test_gloo_world2_matches_oracle(tmp_path, max_sweeps):
+    import torch.multiprocessing as mp
+
+    n, seed, eps = 1000, 3, 1e-9
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_gloo_worker, args=(2, _free_port(), n, seed, eps, max_sweeps, out), nprocs=2, join=True)
+    r = np.load(out)
+    g = orc.build_knn_graph(orc.generate_instance(n, seed), 10)
+    lam, rep = orc.solve_duals(g, eps=eps, max_sweeps=max_sweeps)
+    assert int(r["sweeps"]) == rep["sweeps"]
+    assert bool(r["conv"]) == rep["converged"]
+    assert float(r["fmax"]) == rep["final_max_abs_delta"]
+    assert np.array_equal(r["lam"], lam)
+    assert len(r["record"]) >= rep["sweeps"]
+
+
+def test_schedule_chunk_boundaries():
+    """Converging exactly at a chunk boundary and mid-chunk returns that sweep's vector."""
+    from paper_2011_08170_b200.sharded import LocalComm, run_sharded_jacobi
+
+    g = orc.build_knn_graph(orc.generate_instance(300, 5), 10)
+    lam_ref, rep = orc.solve_duals(g, eps=1e-9)
+    for world in (1, 3):
+        stride = (g.n + world - 1) // world
+        fns = []
+        for r in range(world):
+            b, e = min(g.n, r * stride), min(g.n, (r + 1) * stride)
+            nb, cost = _shard_rows(g, b, e)
+            fns.append(_numpy_sweep(nb, cost, b, e))
+        for chunk in (1, 2, rep["sweeps"], rep["sweeps"] - 1, 64):
+            lam0 = torch.zeros(stride * world, dtype=torch.float64)
+            lam0[: g.n] = torch.from_numpy(orc.initial_state(g))
+            res = run_sharded_jacobi(fns, LocalComm(world), stride, lam0, 1e-9 * g.mean_cost(), 20000, chunk)
+            assert res.sweeps == rep["sweeps"] and res.converged
+            assert np.array_equal(res.lam_full[: g.n].numpy(), lam_ref)
+
+
+# ----------------------------------------------------------------------------------- GPU
+def _gpu_graph(n, seed):
+    import paper_2011_08170_b200 as f2m
+
+    return f2m.build_knn_graph(f2m.generate_instance(n, seed), 10)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_local_shards_match_single_gpu(world):
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_sharded
+
+    g = _gpu_graph(10000, 1)
+    st, rep = f2m.solve_duals(g)
+    lam, srep = solve_duals_sharded(g, LocalComm(world), chunk=16)
+    assert srep["sweeps"] == rep["sweeps"] == 3165
+    assert srep["converged"] and rep["converged"]
+    assert srep["final_max_abs_delta"] == rep["final_max_abs_delta"]
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
+def test_local_shards_truncated_matches_jacobi_sweeps():
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_sharded
+
+    g = _gpu_graph(5000, 2)
+    st = f2m.make_initial_state(g)
+    rec, _ = f2m.jacobi_sweeps(g, st, 45)
+    lam, srep = solve_duals_sharded(g, LocalComm(4), max_sweeps=45, chunk=8, threshold=-1.0)
+    assert srep["sweeps"] == 45 and not srep["converged"]
+    assert np.array_equal(lam, np.asarray(st.lam))
+    assert np.array_equal(np.asarray(srep["record"]), np.asarray(rec))
+
+
+@pytest.mark.gpu
+def test_nccl_world1_matches_single_gpu():
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import TorchDistComm, solve_duals_sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = _gpu_graph(3000, 4)
+        st, rep = f2m.solve_duals(g)
+        lam, srep = solve_duals_sharded(g, TorchDistComm(), chunk=32)
+        assert srep["sweeps"] == rep["sweeps"]
+        assert np.array_equal(lam, np.asarray(st.lam))
+    finally:
+        dist.destroy_process_group()
