@@ -110,3 +110,10 @@ if master is not None and (master > 0).any():
     if need is not None:
         wait = need - master[:-7, None]
         print(f"        decision(k+7) - verdict(k): median {np.median(wait):.0f} ns (negative = CTA waited)")
+if own is not None:
+    print("worst CTAs, per-phase medians relative to top (ns) and clock64 cycles:")
+    for c in np.argsort(-np.nan_to_num(bw))[:4].tolist() + [int(np.argsort(np.nan_to_num(bw))[G // 2])]:
+        ph = {names[p]: int(np.median(tt[:, c, p] - tt[:, c, 0])) for p in (2, 3, 4, 8, 7, 10, 11, 5, 6)}
+        cyc = {k: int(np.median(t[:, c, p])) for k, p in (("rowload", 12), ("rowscan", 13), ("publish", 14), ("bar2end", 15))}
+        spread = np.percentile(tt[:, c, 7] - tt[:, c, 2], [10, 50, 90]).astype(int).tolist()
+        print(f"  CTA {c}: {ph} {cyc} post-halo p10/50/90 {spread}")
