@@ -1185,6 +1185,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   const int bo = a.boff[c] - nint;
   const int bstart = min((s_int - s_lo) * 32, own);  // boundary phase: local [bstart, own)
   const int nbnd = own - bstart;
+  // boundary row of this thread (per batch of cthreads rows): the rotation starts at the first
+  // warp with the fewest interior slices, so boundary work lands on the least-loaded warps
+  const int brow = (tid - ((s_int - s_lo) % ncw) * 32 + cthreads) % cthreads;
   const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
   const int64_t slot0 = a.sptr[s_lo];
   const int nslots = (int)(a.sptr[s_hi] - slot0);
@@ -1348,11 +1351,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     double pv[B + 1];
 #pragma unroll
     for (int i = 0; i <= B; ++i) pv[i] = CUDART_INF;
-    if (RES && a.split && tid < nbnd) {
-      const int lp = bstart + tid, p = p0 + lp;
+    if (RES && a.split && brow < nbnd) {
+      const int lp = bstart + brow, p = p0 + lp;
       const int2 sw2 = slc[(p >> 5) - s_lo];
       const int lb = sw2.x + (p & 31);
-      const int jo = sw2.y - nh_s[tid];
+      const int jo = sw2.y - nh_s[brow];
       const double lv = lam[lp];
       for (int jj = 0; jj < jo; jj += 4) {
         int li[4];
@@ -1387,8 +1390,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     {
       unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
       for (int base = 0; base < nbnd; base += cthreads) {
-        if (base + warp * 32 >= nbnd) break;  // warp-uniform: no row for this warp
-        const int node = base + tid;
+        if (base + (brow & ~31) >= nbnd) break;  // warp-uniform: no row for this warp
+        const int node = base + brow;
         if (node < nbnd) {
           const int lp = bstart + node, p = p0 + lp;
           const int2 sw2 = slc[(p >> 5) - s_lo];
