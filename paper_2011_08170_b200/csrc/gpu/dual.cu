@@ -1506,9 +1506,10 @@ static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t 
   F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
 }
 
-// Resident (smem) layout: 512 threads per CTA (14 compute warps + 2 sync warps) so that ptxas has
-// 128 registers to keep a row's loads in flight; the streaming layout keeps 1024 threads for
-// memory-level parallelism.
+// Resident (smem) layout: 640 threads per CTA (18 compute warps + 2 sync warps, 96 registers):
+// measured best against 512 / 768 / 896 / 1024 — more warps hide more latency until ptxas'
+// register budget (65536 / threads) forces it to serialise each row's load chain. The streaming layout keeps 1024
+// threads for memory-level parallelism.
 template <bool RES, int NT>
 static void dispatch_sweep5(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
   switch (b) {
@@ -1702,13 +1703,16 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       static int nt = -1;
       if (nt < 0) {
         const char* e = std::getenv("F2M_SWEEP_NT");
-        nt = (e && std::atoi(e) == 1024) ? 1024 : 512;
+        nt = e ? std::atoi(e) : 640;
+        if (nt != 512 && nt != 768 && nt != 1024) nt = 640;
       }
       g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg.b) + (t.resident ? ", resident, " : ", streaming, ") +
                           std::to_string(t.resident ? nt : 1024) + "> (persistent: " + std::to_string(G) +
                           " partition CTAs + 1 convergence-master CTA, LL halo exchange, " +
                           std::to_string(t.smem_bytes) + " B smem/CTA)";
       if (t.resident && nt == 512) dispatch_sweep5<true, 512>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+      else if (t.resident && nt == 640) dispatch_sweep5<true, 640>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+      else if (t.resident && nt == 768) dispatch_sweep5<true, 768>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       else if (t.resident) dispatch_sweep5<true, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       else dispatch_sweep5<false, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       launched("gdp_sweep5");
