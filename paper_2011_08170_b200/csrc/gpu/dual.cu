@@ -1993,38 +1993,41 @@ __global__ void __launch_bounds__(256) k_dual_chunks(int n, int64_t m, int nchun
                                                      const double* __restrict__ cost,
                                                      const double* __restrict__ lam,
                                                      double* __restrict__ parts) {
+  // one warp per chunk; the 32 lanes stage 256 terms of the chunk in shared memory, lane 0 adds
+  // them in order (the reference's per-chunk sequential sum, combined in chunk order later)
+  __shared__ double tile[8][256];
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int wl = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nchunks_node + nchunks_edge) return;
+  const bool node = w < nchunks_node;
+  const int64_t b = node ? (int64_t)w * kNodeChunk : (int64_t)(w - nchunks_node) * kEdgeChunk;
+  const int64_t e = node ? min64(n, b + kNodeChunk) : min64(m, b + kEdgeChunk);
   double acc = 0.0;
-  if (w < nchunks_node) {
-    // node chunk: acc += lambda[v] for v in chunk, in order (dual.cpp:96-100)
-    const int64_t b = (int64_t)w * kNodeChunk, e = min64(n, b + kNodeChunk);
-    for (int64_t base = b; base < e; base += 32) {
-      const int64_t v = base + lane;
-      const double val = v < e ? lam[perm[v]] : 0.0;
-      const int cnt = (int)min64(32, e - base);
-      for (int i = 0; i < cnt; ++i) {
-        const double x = __shfl_sync(0xffffffffu, val, i);
-        if (lane == 0) acc = dadd(acc, x);
+  for (int64_t base = b; base < e; base += 256) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t i = base + lane + 32 * k;
+      double v = 0.0;
+      if (i < e) {
+        if (node) {
+          v = lam[perm[i]];  // acc += lambda[v] (dual.cpp:96-100)
+        } else {
+          // if (v_e < 0) acc += v_e, v_e = (c - l_u) - l_v (dual.cpp:101-109). Adding +0.0 for the
+          // others is exact: acc is +0.0 or a negative non-zero sum, both unchanged by +0.0.
+          const double x = dsub(dsub(cost[i], lam[perm[eu[i]]]), lam[perm[ev[i]]]);
+          v = x < 0.0 ? x : 0.0;
+        }
       }
+      tile[wl][lane + 32 * k] = v;
     }
-  } else {
-    // edge chunk: if (v_e < 0) acc += v_e, v_e = (c - l_u) - l_v (dual.cpp:101-109)
-    const int c = w - nchunks_node;
-    const int64_t b = (int64_t)c * kEdgeChunk, e = min64(m, b + kEdgeChunk);
-    for (int64_t base = b; base < e; base += 32) {
-      const int64_t ed = base + lane;
-      double val = 0.0;
-      if (ed < e) val = dsub(dsub(cost[ed], lam[perm[eu[ed]]]), lam[perm[ev[ed]]]);
-      unsigned neg = __ballot_sync(0xffffffffu, ed < e && val < 0.0);
-      while (neg) {
-        const int i = __ffs(neg) - 1;
-        neg &= neg - 1;
-        const double x = __shfl_sync(0xffffffffu, val, i);
-        if (lane == 0) acc = dadd(acc, x);
-      }
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = (int)min64(256, e - base);
+#pragma unroll 8
+      for (int k = 0; k < cnt; ++k) acc = dadd(acc, tile[wl][k]);
     }
+    __syncwarp();
   }
   if (lane == 0) parts[w] = acc;
 }

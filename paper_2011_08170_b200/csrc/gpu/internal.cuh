@@ -233,7 +233,7 @@ void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, dou
 double objective_device(const f2m_graph& g, const double* d_x);
 void verify_device(const f2m_graph& g, const double* d_x, double objective,
                    const double* d_lam_pos, f2m_verification& rep, int32_t* h_nodes,
-                   double* h_sums, int32_t* h_vals, int64_t capacity);
+                   double* h_sums, int32_t* h_vals, int64_t capacity, const double* dual_known = nullptr);
 
 // persistent sweep launch geometry (dual.cu)
 int sweep_grid_ctas(int dev);

@@ -403,7 +403,7 @@ double objective_device(const f2m_graph& g, const double* d_x) {
 
 void verify_device(const f2m_graph& g, const double* d_x, double objective, const double* d_lam_pos,
                    f2m_verification& rep, int32_t* h_nodes, double* h_sums, int32_t* h_vals,
-                   int64_t capacity) {
+                   int64_t capacity, const double* dual_known) {
   const Topology& t = *g.topo;
   cudaStream_t s = t.stream;
   const int n = t.n;
@@ -440,7 +440,9 @@ void verify_device(const f2m_graph& g, const double* d_x, double objective, cons
   rep.violated_count = nbad;
   rep.value_violation_count = vbad;
   rep.feasible = nbad == 0 && vbad == 0;
-  rep.duality_gap = objective - dual_objective_device(g, d_lam_pos, 2);  // dual_objective(graph, state)
+  // dual_objective(graph, state) (primal.cpp:274); solve_duals already computed it for the same
+  // graph, lambda and b when the caller passes it in
+  rep.duality_gap = objective - (dual_known ? *dual_known : dual_objective_device(g, d_lam_pos, 2));
 }
 
 }  // namespace f2mgpu

@@ -76,7 +76,10 @@ static void full_solve_graph_device(const f2m_graph& g, const f2m_run_config& rc
     // certify against the unperturbed costs (solve.cpp:74-83)
     const double objective = objective_device(g, x.get());
     f2m_verification ver{};
-    verify_device(g, x.get(), objective, lam.get(), ver, nullptr, nullptr, nullptr, 0);
+    // restart 0 solved on g itself with b = 2: its report already holds dual_objective(g, lambda)
+    const bool same = jit == nullptr && rc.engine.b == 2;
+    verify_device(g, x.get(), objective, lam.get(), ver, nullptr, nullptr, nullptr, 0,
+                  same ? &conv.dual_value : nullptr);
     t_extract += seconds_since(ts);
     const double scale = 1.0 + std::fabs(objective);
     if (ver.feasible && ver.duality_gap <= rc.gap_tol * scale) {
