@@ -30,6 +30,14 @@ const cudaDeviceProp& device_props(int dev) {
     auto p = std::make_unique<cudaDeviceProp>();
     F2M_CUDA(cudaGetDeviceProperties(p.get(), dev));
     cache[dev] = std::move(p);
+    // Scratch buffers are stream-ordered allocations (DBuf). Keep freed memory in the device's
+    // pool instead of returning it to the driver at every synchronisation (the default release
+    // threshold is 0), so repeated solves do not pay cudaMalloc-class latencies.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
   }
   return *cache[dev];
 }
@@ -48,6 +56,7 @@ Topology::~Topology() {
 }
 
 std::shared_ptr<Topology> make_topology(int n, int dev) {
+  (void)device_props(dev);  // first use of the device configures its memory pool
   auto t = std::make_shared<Topology>();
   t->dev = dev;
   t->n = n;

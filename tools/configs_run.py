@@ -1,0 +1,35 @@
+"""Time-to-solve of every BASELINE.json config on one GPU (certified full solves through the C ABI),
+next to the reference's sweep counts where SURVEY.md §6 / tests/golden record them."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2011_08170_b200 as f2m  # noqa: E402
+
+CONFIGS = [
+    ("uniform 1k seed 1", "u", 1000, 1, 1e-9),
+    ("uniform 10k seed 1", "u", 10000, 1, 1e-9),
+    ("uniform 100k seed 1", "u", 100000, 1, 1e-9),
+    ("uniform 100k seed 31337 eps 1e-8 (c7)", "u", 100000, 31337, 1e-8),
+    ("uniform 200k seed 1", "u", 200000, 1, 1e-9),
+    ("clustered 200k seed 1", "c", 200000, 1, 1e-9),
+    ("uniform 2M seed 1", "u", 2000000, 1, 1e-9),
+]
+only = sys.argv[1:] or None
+for name, kind, n, seed, eps in CONFIGS:
+    if only and not any(o in name for o in only):
+        continue
+    gen = f2m.generate_clustered_instance if kind == "c" else f2m.generate_instance
+    xy = gen(n, seed).points_array()
+    f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=200000) if n <= 200000 else None  # warm-up
+    t0 = time.perf_counter()
+    r = f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=400000)
+    wall = time.perf_counter() - t0
+    ms, sw = f2m.last_sweep_kernel()
+    print(json.dumps({"config": name, "n": n, "m": int(r["graph"].m), "wall_s": wall, "t_total": r["t_total"],
+                      "t_knn": r["t_knn"], "t_duals": r["t_duals"], "t_extract": r["t_extract"],
+                      "sweeps": r["sweeps"], "restarts": r["restarts"], "objective": r["objective"],
+                      "gap": r["gap"], "us_per_sweep": 1e3 * ms / max(sw, 1),
+                      "kernel": f2m.last_sweep_kernel_desc()}), flush=True)
