@@ -355,22 +355,25 @@ PYBIND11_MODULE(_f2m, m) {
         const int n = static_cast<int>(xy.size() / 2);
         const int per = std::max(3, std::min(k, n - 1));
         f2m_run_config rc = run_config_c(k, 0.5, eps, max_sweeps, "jacobi", tol, max_restarts, seed, 1e-6, 1e-7);
-        std::vector<double> x(static_cast<size_t>(n) * per + 1), lam(static_cast<size_t>(std::max(n, 1)));
+        // results land directly in (uninitialised) numpy buffers: m <= n * per (each node adds at
+        // most `per` candidate edges), the edge-value view is trimmed to m afterwards (no copy)
+        py::array_t<double> x(static_cast<py::ssize_t>(n) * per + 1);
+        py::array_t<double> lam(static_cast<py::ssize_t>(std::max(n, 1)));
+        double* px = x.mutable_data();
+        double* pl = lam.mutable_data();
         f2m_solve_outcome o{};
         f2m_graph* g = nullptr;
         const double* p = xy.data();
         int st;
         {
           py::gil_scoped_release release;
-          st = f2m_full_solve(n, p, rounded ? 1 : 0, &rc, x.data(), lam.data(), &o, &g);
+          st = f2m_full_solve(n, p, rounded ? 1 : 0, &rc, px, pl, &o, &g);
         }
         f2m::check(st);
         f2m::Graph graph = f2m::Graph::adopt(g);
-        x.resize(static_cast<size_t>(graph.edge_count()));
-        lam.resize(static_cast<size_t>(n));
         py::dict d = outcome_dict(o);
-        d["value"] = py::array_t<double>(static_cast<py::ssize_t>(x.size()), x.data());
-        d["duals"] = py::array_t<double>(static_cast<py::ssize_t>(lam.size()), lam.data());
+        d["value"] = x[py::slice(0, static_cast<py::ssize_t>(graph.edge_count()), 1)];
+        d["duals"] = lam[py::slice(0, n, 1)];
         d["graph"] = graph;
         return d;
       },
