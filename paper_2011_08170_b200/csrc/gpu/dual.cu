@@ -195,6 +195,106 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep(SweepArgs a, Swe
 }
 
 
+// warp max of non-negative doubles (NaN skipped), as warp_max_nonneg below
+__device__ __forceinline__ unsigned long long warp_max_nonneg_ap(double x) {
+  const unsigned long long v = x == x ? (unsigned long long)__double_as_longlong(x) : 0ull;
+  const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
+}
+
+// ---------------------------------------------------------------- all-pairs Jacobi sweep
+// Complete graphs (build_knn_graph with k >= n-1, graph.cpp:175) whose costs are the points'
+// distances: every cost is recomputed on the fly as distance() does it (instance.cpp:126-141:
+// sqrt(dx*dx + dy*dy) without FMA, rounded mode floor(d + 0.5)) instead of streaming the
+// n(n-1)/2-edge CSR — the FP64-pipe-bound variant of SURVEY §8(f). All points and the frozen
+// multipliers sit in shared memory; one warp per node scans its n-1 partners (lane-strided) and
+// the lanes' top lists are merged with shuffles. Same sweep/convergence protocol as k_gdp_sweep.
+constexpr int kAllPairsThreads = 512;
+constexpr int kAllPairsMaxN = 8192;
+
+struct AllPairsArgs {
+  int n;
+  const double2* __restrict__ pts;  // position order
+  int rounded;
+  double* lam0;
+  double* lam1;
+  double eta;
+  int update;
+  double threshold;
+  int max_sweeps;
+  double* record;
+};
+
+template <int B>
+__global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairsArgs a, SweepCtl* ctl) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[kAllPairsThreads / 32];
+  __shared__ double s_gmax;
+  double2* pts = reinterpret_cast<double2*>(smem);
+  double* lam = reinterpret_cast<double*>(pts + a.n);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < a.n; i += blockDim.x) pts[i] = a.pts[i];
+  int sweep = 0;
+  double gmax = INFINITY;
+  bool converged = false;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    const double* lin = (sweep & 1) ? a.lam1 : a.lam0;
+    double* lout = (sweep & 1) ? a.lam0 : a.lam1;
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) lam[i] = __ldcg(lin + i);
+    __syncthreads();
+    double mx = 0.0;
+    for (int v = blockIdx.x * nwarps + warp; v < a.n; v += gridDim.x * nwarps) {
+      const double2 pv = pts[v];
+      const double lv = lam[v];
+      double s[B + 1];
+#pragma unroll
+      for (int i = 0; i <= B; ++i) s[i] = CUDART_INF;
+      for (int u = lane; u < a.n; u += 32) {
+        if (u == v) continue;
+        const double2 pu = pts[u];
+        const double dx = dsub(pv.x, pu.x), dy = dsub(pv.y, pu.y);
+        double c = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+        if (a.rounded) c = floor(dadd(c, 0.5));
+        topk_insert<B>(s, dsub(dsub(c, lv), lam[u]));
+      }
+      warp_topk_merge<B>(s);
+      if (lane == 0) {
+        const double d = delta_of<B>(s, a.update);
+        lout[v] = dadd(lv, dmul(a.eta, d));
+        const double ad = fabs(d);
+        mx = mx < ad ? ad : mx;
+      }
+    }
+    const unsigned long long wm = warp_max_nonneg_ap(mx);
+    if (lane == 0) red[warp] = __longlong_as_double((long long)wm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bm = 0.0;
+      for (int w = 0; w < nwarps; ++w) bm = bm < red[w] ? red[w] : bm;
+      if (blockIdx.x == 0) ctl->maxbits[(sweep + 1) % 3] = 0ull;
+      atomicMax(&ctl->maxbits[sweep % 3], (unsigned long long)__double_as_longlong(bm));
+      grid_barrier(&ctl->bar, (unsigned)(sweep + 1) * gridDim.x, &ctl->error);
+      s_gmax = __longlong_as_double((long long)atomicAdd(&ctl->maxbits[sweep % 3], 0ull));
+      if (blockIdx.x == 0 && a.record) a.record[sweep] = s_gmax;
+    }
+    __syncthreads();
+    gmax = s_gmax;
+    if (ctl->error) break;
+    if (gmax <= a.threshold) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->sweeps = sweep;
+    ctl->converged = converged ? 1 : 0;
+    ctl->final_max = gmax;
+  }
+}
+
 // ---------------------------------------------------------------- persistent Jacobi sweep v3
 // Neighbour-synchronised persistent kernel (no grid barrier).
 //  * CTA c owns a contiguous, degree-balanced slice range; inside it interior nodes (all
@@ -1596,7 +1696,59 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
   F2M_CUDA(cudaEventCreate(&e1));
   int error = 0, sweeps = 0, converged = 0, outbuf = 0;
   double final_max = INFINITY;
-  if (use_v1(t)) {
+  static int allpairs_env = -1;  // F2M_ALLPAIRS=0 forces the CSR kernels for complete graphs
+  if (allpairs_env < 0) {
+    const char* e = std::getenv("F2M_ALLPAIRS");
+    allpairs_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (g.allpairs && allpairs_env && t.n <= kAllPairsMaxN) {
+    const double2* pts = g.pts_pos.get();
+    DBuf<SweepCtl> ctl(1, s);
+    F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl), s));
+    AllPairsArgs ap;
+    ap.n = t.n;
+    ap.pts = pts;
+    ap.rounded = g.rounded;
+    ap.lam0 = d_lam0;
+    ap.lam1 = d_lam1;
+    ap.eta = cfg.eta;
+    ap.update = cfg.update;
+    ap.threshold = defer_eps > 0.0 ? defer_eps * graph_mean(g) : threshold;
+    ap.max_sweeps = max_sweeps;
+    ap.record = d_record;
+    const size_t smem = (size_t)t.n * (sizeof(double2) + sizeof(double));
+    const int ctas = std::min(sweep_grid_ctas(t.dev), std::max(1, (t.n + 15) / 16));
+    g_last_sweep_desc = "k_allpairs_sweep<b=" + std::to_string(cfg.b) + "> (" + std::to_string(ctas) +
+                        " CTAs x 512, costs recomputed from the points, " + std::to_string(smem) + " B smem/CTA)";
+    F2M_CUDA(cudaEventRecord(e0, s));
+    SweepCtl* ctlp = ctl.get();
+    void* args[] = {(void*)&ap, (void*)&ctlp};
+    switch (cfg.b) {
+#define F2M_AP(BB)                                                                                          \
+  case BB: {                                                                                                \
+    auto fn = k_allpairs_sweep<BB>;                                                                         \
+    F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kAllPairsThreads), args, smem, s)); \
+  } break;
+      F2M_AP(1) F2M_AP(2) F2M_AP(3) F2M_AP(4) F2M_AP(5) F2M_AP(6) F2M_AP(7)
+      default: {
+        auto fn = k_allpairs_sweep<8>;
+        F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kAllPairsThreads), args, smem, s));
+      } break;
+#undef F2M_AP
+    }
+    launched("allpairs_sweep");
+    F2M_CUDA(cudaEventRecord(e1, s));
+    SweepCtl h;
+    F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    error = h.error;
+    sweeps = h.sweeps;
+    converged = h.converged;
+    final_max = h.final_max;
+    outbuf = (h.sweeps & 1) ? 1 : 0;
+  } else if (use_v1(t)) {
     DBuf<SweepCtl> ctl(1, s);
     F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl), s));
     SweepArgs a;

@@ -174,6 +174,12 @@ struct f2m_graph {
   mutable double mean_cost = 0.0;
   mutable bool mean_known = false;
   f2mgpu::DBuf<double> approx_sum;  // [1] parallel sum of the costs (device)
+  // Complete graph whose costs are the points' distances (build_knn_graph with k >= n-1,
+  // graph.cpp:175): the sweeps can recompute every cost on the fly from the points instead of
+  // streaming the n(n-1)/2-edge CSR (all-pairs mode). Points in position order.
+  f2mgpu::DBuf<double2> pts_pos;
+  int rounded = 0;
+  bool allpairs = false;
 };
 
 namespace f2mgpu {

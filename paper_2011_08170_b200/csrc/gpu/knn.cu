@@ -228,6 +228,15 @@ __global__ void k_morton(int n, const int32_t* __restrict__ cell_of, const GridP
   idx[i] = i;
 }
 
+__global__ void k_points_by_position(int n, const double* __restrict__ xy, const int32_t* __restrict__ iperm,
+                                     double2* __restrict__ pts) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    const int v = iperm[p];
+    pts[p] = make_double2(xy[2 * v], xy[2 * v + 1]);
+  }
+}
+
 __global__ void k_invert(int n, const int32_t* __restrict__ iperm, int32_t* __restrict__ perm) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) perm[iperm[p]] = p;
@@ -354,6 +363,13 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   }
   finalize_topology(t);
   attach_costs(*g);
+  if (per_node == n - 1) {  // complete graph: keep the points for the all-pairs sweep
+    g->pts_pos.alloc(n, s);
+    k_points_by_position<<<grid_for(n, 256), 256, 0, s>>>(n, d_xy, t.iperm.get(), g->pts_pos.get());
+    launched("points_by_position");
+    g->rounded = rounded;
+    g->allpairs = true;
+  }
   return g.release();
 }
 

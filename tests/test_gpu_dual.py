@@ -256,3 +256,46 @@ def test_grid_barrier_kernel_fallback_parity():
     sweeps, dual, digest = json.loads(out.stdout.strip().splitlines()[-1])
     meta, _ = golden("u10k_s1")
     assert sweeps == meta["sweeps"] and dual == meta["dual_value"] and digest == meta["sha256"]["lam_final"]
+
+
+# ------------------------------------------------------------------ all-pairs (complete graphs)
+@pytest.mark.parametrize("n,seed,rounded", [(8, 1, False), (60, 2, False), (300, 3, True), (1200, 4, False)])
+def test_allpairs_complete_graph_matches_oracle(f2m, n, seed, rounded):
+    """k >= n-1 builds the complete graph (graph.cpp:175); its sweeps recompute every cost from
+    the points (k_allpairs_sweep). lambda, sweep count, final max|delta|, dual value and the
+    per-sweep maxima must equal the C oracle's CSR solve bit for bit."""
+    from oracle import oracle as orc
+
+    inst = f2m.generate_instance(n, seed)
+    if rounded:
+        inst.mode = f2m.DistanceMode.EUC2D_ROUNDED
+    g = f2m.build_knn_graph(inst, n - 1)
+    assert g.m == n * (n - 1) // 2
+    st, rep = f2m.solve_duals(g, max_sweeps=20000)
+    assert "allpairs" in f2m.last_sweep_kernel_desc()
+    og = orc.build_knn_graph(inst.points_array(), n - 1, rounded=rounded)
+    lam, orep = orc.solve_duals(og, max_sweeps=20000)
+    assert rep["sweeps"] == orep["sweeps"] and rep["converged"] == orep["converged"]
+    assert rep["final_max_abs_delta"] == orep["final_max_abs_delta"]
+    assert rep["dual_value"] == orep["dual_value"]
+    assert np.array_equal(np.asarray(st.lam), lam)
+    # fixed-count sweeps: per-sweep maxima
+    st0 = f2m.make_initial_state(g)
+    mx, _ = f2m.jacobi_sweeps(g, st0, 25)
+    lam0 = orc.initial_state(og)
+    for k in range(25):
+        m_k, _ = orc.jacobi_sweep(og, lam0)
+        assert mx[k] == m_k
+    assert np.array_equal(np.asarray(st0.lam), lam0)
+
+
+def test_allpairs_full_solve_certified(f2m):
+    """full_solve on a complete graph: all-pairs sweeps, CSR extraction, same certificate."""
+    from oracle import oracle as orc
+
+    inst = f2m.generate_instance(400, 9)
+    r = f2m.full_solve_arrays(inst.points_array(), k=399)
+    og = orc.build_knn_graph(inst.points_array(), 399)
+    ref = orc.full_solve_graph(og, k=399)
+    assert r["sweeps"] == ref["sweeps"] and r["objective"] == ref["objective"]
+    assert np.array_equal(r["value"], ref["value"])
