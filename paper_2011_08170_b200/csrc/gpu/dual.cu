@@ -733,7 +733,6 @@ struct Sweep4Args {
   const uint8_t* __restrict__ row_nhalo; // v5: halo slots per row
   unsigned poll_ns;          // v5: sync-warp back-off between unproductive halo polls
   int runahead;              // v5: stage the next sweep's halo while this sweep computes
-  int debug;                 // timing experiments only (F2M_SWEEP_DEBUG): 1 = no halo wait
   int split;                 // v5: scan boundary rows' own-CTA slots before the halo arrives
   // deferred threshold (v5): defer_eps > 0 -> threshold = defer_eps * mean_cost, where the master
   // CTA computes mean_cost (sequential sum of cost[0..m) / m, graph.cpp:47-49) during the solve
@@ -1333,7 +1332,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
       const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
       const uint64_t t0 = globaltimer_ns();
-      bool quit = a.debug == 1 && s > 0;  // timing experiment: do not wait for the halo (WRONG results)
+      bool quit = false;
       for (int base = sw * 32; base < nh && !quit; base += 64 * 8) {
         unsigned pend = 0;
 #pragma unroll
@@ -1534,7 +1533,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           }
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (lp >= nint && a.debug != 2) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
           gout[p] = nl;
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
@@ -1826,10 +1825,8 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.m = t.m;
     a.approx_sum = g.approx_sum.get();
     a.mean_out = mean_out.get();
-    a.debug = 0;
     a.split = 1;
     if (const char* e = std::getenv("F2M_SPLIT")) a.split = std::atoi(e);
-    if (const char* e = std::getenv("F2M_SWEEP_DEBUG")) a.debug = std::atoi(e);
     if (const char* e = std::getenv("F2M_RUNAHEAD")) a.runahead = std::atoi(e);
     if (const char* e = std::getenv("F2M_POLL_NS")) a.poll_ns = (unsigned)std::max(0, std::atoi(e));
     a.cmax = cmax.get();
