@@ -20,8 +20,9 @@ generator), i.e. the reference's full_solve (solve.cpp:101-106).
 --impl reference runs only that reference leg (rank 0), printing the same JSON line shape.
 Multi-GPU (torchrun, N>1): every rank solves its own replica of the headline instance (weak
 scaling, no data-path collective): that is `value`. The line also carries `sharded_2m`: the
-node-sharded engine on the 2M-city instance split across the N ranks (NCCL
-all-gather of lambda per sweep), per-sweep device time over a fixed sweep count.
+node-sharded engine on the 2M-city instance split across the N ranks (halo
+exchange of the multipliers other ranks read, NCCL all-to-all per sweep), per-sweep device time
+over a fixed sweep count.
 """
 from __future__ import annotations
 
@@ -204,45 +205,35 @@ def sharded_leg(args, ws, rank, local, dev, n=2_000_000, sweeps=256, chunk=32):
     import torch
 
     import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200 import _f2m
-    from paper_2011_08170_b200.sharded import ShardedJacobi, TorchDistComm
+    from paper_2011_08170_b200.sharded import TorchDistComm, make_halo_schedule
 
-    if ws > 1:
-        comm = TorchDistComm()
-    else:
-        import torch.distributed as dist
-        if not dist.is_initialized():
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29541")
-            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
-        comm = TorchDistComm()
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    comm = TorchDistComm()
     g = f2m.build_knn_graph(f2m.generate_instance(n, SEED, 1000.0), K)
-    sh = _f2m.shard_create(g, comm.rank, comm.world)
-    stride = sh.info()["stride"]
-    lam0 = torch.zeros(stride * comm.world, dtype=torch.float64, device=dev)
-    _f2m.initial_state_positions(g, lam0.data_ptr(), 2, "local-midpoint", torch.cuda.current_stream(dev).cuda_stream)
-
-    def fn(lf, out, bits):
-        sh.sweep(lf.data_ptr(), out.data_ptr(), bits.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
-
-    sched = ShardedJacobi([fn], comm, stride, dev, chunk)
-    sched.run(lam0, -1.0, 2 * chunk)  # eager chunk + CUDA-graph capture
+    sched, lam0, meta = make_halo_schedule(g, comm, chunk=chunk)
+    sched.run([lam0], -1.0, 2 * chunk)  # eager chunk + CUDA-graph capture
     torch.cuda.synchronize()
-    comm.dist.barrier()
+    dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sched.run(lam0, -1.0, sweeps)
+    sched.run([lam0], -1.0, sweeps)
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    comm.dist.all_reduce(ms, op=comm.dist.ReduceOp.MAX)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     per_us = float(ms.item()) * 1e3 / sweeps
     return {"workload": f"random-uniform {n} cities (seed {SEED}), k={K}, node-sharded x{comm.world}, "
-                        f"{sweeps} Jacobi sweeps (fixed count), NCCL all-gather of lambda per sweep",
+                        f"{sweeps} Jacobi sweeps (fixed count), halo exchange (NCCL all-to-all) per sweep",
             "n": n, "m": int(g.m), "ranks": comm.world, "us_per_sweep": per_us,
             "gdp_iterations_per_s": 1e6 / per_us,
             "algorithmic_GBps": g.sweep_bytes() / (per_us * 1e-6) / 1e9,
-            "kernel": "k_shard_sweep<2> + ncclAllGather + chunked ncclAllReduce(max), CUDA-graph replay"}
+            "halo_values_per_sweep": meta["halo_values_per_sweep"],
+            "kernel": "k_shard_sweep<2> + halo pack / ncclAllToAll / unpack + chunked ncclAllReduce(max), "
+                      "CUDA-graph replay"}
 
 
 def run_gpu(args):

@@ -273,6 +273,13 @@ int f2m_shard_sweep(const f2m_shard* s, const f2m_engine_config* cfg, const doub
 int f2m_initial_state_positions(const f2m_graph* g, const f2m_engine_config* cfg, double* d_lam_pos,
                                 void* stream);
 int f2m_positions_to_ids(const f2m_graph* g, const double* d_pos, double* d_ids, void* stream);
+/* The device's spatial order: position[v] of every node id v (host array, n int32). Ranks use it
+ * to plan the halo exchange of the sharded solve. */
+int f2m_graph_positions(const f2m_graph* g, int32_t* position);
+/* Halo exchange helpers on the caller's stream (device arrays): d_dst[i] = d_src[d_idx[i]]
+ * (pack) and d_dst[d_idx[i]] = d_src[i] (unpack), i < count. */
+int f2m_gather_f64(const double* d_src, const int32_t* d_idx, double* d_dst, int64_t count, void* stream);
+int f2m_scatter_f64(const double* d_src, const int32_t* d_idx, double* d_dst, int64_t count, void* stream);
 int f2m_ids_to_positions(const f2m_graph* g, const double* d_ids, double* d_pos, void* stream);
 
 /* ---- instrumentation (bench.py / tests) ----------------------------------------------- */

@@ -101,6 +101,18 @@ __global__ void k_perm_gather(int n, const double* __restrict__ src, const int32
   if (i < n) dst[i] = src[idx[i]];
 }
 
+__global__ void k_pack(int64_t count, const double* __restrict__ src, const int32_t* __restrict__ idx,
+                       double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = src[idx[i]];
+}
+
+__global__ void k_unpack(int64_t count, const double* __restrict__ src, const int32_t* __restrict__ idx,
+                         double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < count) dst[idx[i]] = src[i];
+}
+
 }  // namespace f2mgpu
 
 using namespace f2mgpu;
@@ -202,5 +214,29 @@ extern "C" int f2m_ids_to_positions(const f2m_graph* g, const double* d_ids, dou
     // pos[p] = ids[iperm[p]]
     k_perm_gather<<<grid_for(t.n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(t.n, d_ids, t.iperm.get(), d_pos);
     launched("ids_to_positions");
+  });
+}
+
+extern "C" int f2m_graph_positions(const f2m_graph* g, int32_t* position) {
+  return guard([&] {
+    const Topology& t = *g->topo;
+    F2M_CUDA(cudaSetDevice(t.dev));
+    if (t.n > 0) F2M_CUDA(cudaMemcpy(position, t.perm.get(), sizeof(int32_t) * t.n, cudaMemcpyDeviceToHost));
+  });
+}
+
+extern "C" int f2m_gather_f64(const double* d_src, const int32_t* d_idx, double* d_dst, int64_t count, void* stream) {
+  return guard([&] {
+    if (count <= 0) return;
+    k_pack<<<grid_for(count, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(count, d_src, d_idx, d_dst);
+    launched("halo_pack");
+  });
+}
+
+extern "C" int f2m_scatter_f64(const double* d_src, const int32_t* d_idx, double* d_dst, int64_t count, void* stream) {
+  return guard([&] {
+    if (count <= 0) return;
+    k_unpack<<<grid_for(count, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(count, d_src, d_idx, d_dst);
+    launched("halo_unpack");
   });
 }

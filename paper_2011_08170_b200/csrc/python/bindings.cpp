@@ -145,6 +145,12 @@ PYBIND11_MODULE(_f2m, m) {
              if (mm) f2m::check(f2m_graph_edges(g.handle(), u.mutable_data(), v.mutable_data(), c.mutable_data()));
              return py::make_tuple(u, v, c);
            })
+      .def("positions",
+           [](const f2m::Graph& g) {
+             py::array_t<int32_t> p(g.node_count());
+             if (g.node_count()) f2m::check(f2m_graph_positions(g.handle(), p.mutable_data()));
+             return p;
+           })
       .def("degrees",
            [](const f2m::Graph& g) {
              py::array_t<int32_t> d(g.node_count());
@@ -459,6 +465,20 @@ PYBIND11_MODULE(_f2m, m) {
                                         reinterpret_cast<double*>(d_ids), reinterpret_cast<void*>(stream)));
       },
       py::arg("graph"), py::arg("d_pos"), py::arg("d_ids"), py::arg("stream") = 0);
+  m.def(
+      "gather_f64",
+      [](std::uintptr_t src, std::uintptr_t idx, std::uintptr_t dst, std::int64_t count, std::uintptr_t stream) {
+        f2m::check(f2m_gather_f64(reinterpret_cast<const double*>(src), reinterpret_cast<const int32_t*>(idx),
+                                  reinterpret_cast<double*>(dst), count, reinterpret_cast<void*>(stream)));
+      },
+      py::arg("src"), py::arg("idx"), py::arg("dst"), py::arg("count"), py::arg("stream") = 0);
+  m.def(
+      "scatter_f64",
+      [](std::uintptr_t src, std::uintptr_t idx, std::uintptr_t dst, std::int64_t count, std::uintptr_t stream) {
+        f2m::check(f2m_scatter_f64(reinterpret_cast<const double*>(src), reinterpret_cast<const int32_t*>(idx),
+                                   reinterpret_cast<double*>(dst), count, reinterpret_cast<void*>(stream)));
+      },
+      py::arg("src"), py::arg("idx"), py::arg("dst"), py::arg("count"), py::arg("stream") = 0);
   m.def(
       "ids_to_positions",
       [](const f2m::Graph& graph, std::uintptr_t d_ids, std::uintptr_t d_pos, std::uintptr_t stream) {

@@ -1,9 +1,10 @@
 """Node-sharded multi-GPU GDP: the sharded solve must be bit-identical to the
 single-process solve for every world size.
 
-CPU (world 2, gloo, two processes): the collective schedule of paper_2011_08170_b200/sharded.py
-(run_sharded_jacobi) driven by a numpy restatement of a shard's Jacobi rows, against the C oracle's
-solve_duals (which is pinned to the reference's golden vectors).
+CPU (world 2, gloo, two processes): the collective schedules of paper_2011_08170_b200/sharded.py
+(all-gather: run_sharded_jacobi; halo exchange: ShardedJacobiHalo) driven by a numpy restatement
+of a shard's Jacobi rows, against the C oracle's solve_duals (pinned to the reference's golden
+vectors).
 GPU: the CUDA shard kernel + the same schedule with in-process shards (LocalComm, worlds 1..8) and
 through torch.distributed/NCCL (world 1), against the persistent one-GPU solver.
 """
@@ -140,7 +141,7 @@ def test_local_shards_match_single_gpu(world):
 
     g = _gpu_graph(10000, 1)
     st, rep = f2m.solve_duals(g)
-    lam, srep = solve_duals_sharded(g, LocalComm(world), chunk=16)
+    lam, srep = solve_duals_sharded(g, LocalComm(world), chunk=16, exchange="allgather")
     assert srep["sweeps"] == rep["sweeps"] == 3165
     assert srep["converged"] and rep["converged"]
     assert srep["final_max_abs_delta"] == rep["final_max_abs_delta"]
@@ -174,7 +175,112 @@ def test_nccl_world1_matches_single_gpu():
     try:
         g = _gpu_graph(3000, 4)
         st, rep = f2m.solve_duals(g)
-        lam, srep = solve_duals_sharded(g, TorchDistComm(), chunk=32)
+        lam, srep = solve_duals_sharded(g, TorchDistComm(), chunk=32, exchange="allgather")
+        assert srep["sweeps"] == rep["sweeps"]
+        assert np.array_equal(lam, np.asarray(st.lam))
+    finally:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ halo exchange
+def _halo_gloo_worker(rank, world, port, n, seed, eps, out_path):
+    import torch.distributed as dist
+
+    from paper_2011_08170_b200.sharded import ShardedJacobiHalo, TorchDistComm, halo_plans
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = orc.build_knn_graph(orc.generate_instance(n, seed), 10)
+        stride = (g.n + world - 1) // world
+        begin, end = min(g.n, rank * stride), min(g.n, (rank + 1) * stride)
+        nb, cost = _shard_rows(g, begin, end)
+        plans = halo_plans(g.n, world, stride, g.eu, g.ev)  # positions == ids on the CPU
+        lam0 = torch.zeros(stride * world, dtype=torch.float64)
+        lam0[: g.n] = torch.from_numpy(orc.initial_state(g))
+
+        def pack(src, idx, dst, count):
+            dst.copy_(src[idx.long()])
+
+        def unpack(src, idx, dst, count):
+            dst[idx.long()] = src
+
+        sched = ShardedJacobiHalo([_numpy_sweep(nb, cost, begin, end)], TorchDistComm(), stride, plans, [rank],
+                                  "cpu", pack, unpack, chunk=5)
+        sweeps, conv, fmax, record, slot = sched.run([lam0], eps * g.mean_cost(), 20000)
+        full = torch.empty(stride * world, dtype=torch.float64)
+        dist.all_gather_into_tensor(full, sched.rings[0][slot][rank * stride:(rank + 1) * stride].contiguous())
+        if rank == 0:
+            np.savez(out_path, lam=full[: g.n].numpy(), sweeps=sweeps, conv=conv, fmax=fmax,
+                     halo=sum(len(p.recv_pos) for p in plans))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_plans_match_neighbourhoods():
+    from paper_2011_08170_b200.sharded import halo_plans
+
+    g = orc.build_knn_graph(orc.generate_instance(500, 8), 10)
+    world = 4
+    stride = (g.n + world - 1) // world
+    plans = halo_plans(g.n, world, stride, g.eu, g.ev)
+    for r in range(world):
+        b, e = r * stride, min(g.n, (r + 1) * stride)
+        need = set()
+        for u, v in zip(g.eu, g.ev):
+            if b <= u < e and not b <= v < e:
+                need.add(int(v))
+            if b <= v < e and not b <= u < e:
+                need.add(int(u))
+        assert plans[r].recv_pos.tolist() == sorted(need)
+        for q in range(world):
+            assert plans[r].send_counts[q] == plans[q].recv_counts[r]
+
+
+def test_gloo_world2_halo_matches_oracle(tmp_path):
+    import torch.multiprocessing as mp
+
+    n, seed, eps = 1000, 3, 1e-9
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_halo_gloo_worker, args=(2, _free_port(), n, seed, eps, out), nprocs=2, join=True)
+    r = np.load(out)
+    g = orc.build_knn_graph(orc.generate_instance(n, seed), 10)
+    lam, rep = orc.solve_duals(g, eps=eps)
+    assert int(r["sweeps"]) == rep["sweeps"] and bool(r["conv"])
+    assert float(r["fmax"]) == rep["final_max_abs_delta"]
+    assert np.array_equal(r["lam"], lam)
+    assert 0 < int(r["halo"]) < n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_local_shards_halo_match_single_gpu(world):
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_sharded
+
+    g = _gpu_graph(10000, 1)
+    st, rep = f2m.solve_duals(g)
+    lam, srep = solve_duals_sharded(g, LocalComm(world), chunk=16, exchange="halo")
+    assert srep["sweeps"] == rep["sweeps"] == 3165
+    assert srep["final_max_abs_delta"] == rep["final_max_abs_delta"]
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
+def test_nccl_world1_halo_matches_single_gpu():
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import TorchDistComm, solve_duals_sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = _gpu_graph(3000, 4)
+        st, rep = f2m.solve_duals(g)
+        lam, srep = solve_duals_sharded(g, TorchDistComm(), chunk=32, exchange="halo")
         assert srep["sweeps"] == rep["sweeps"]
         assert np.array_equal(lam, np.asarray(st.lam))
     finally:

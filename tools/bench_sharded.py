@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--local", type=int, default=0, help="simulate this many shards in one process")
     ap.add_argument("--solve", action="store_true")
+    ap.add_argument("--exchange", default="halo", choices=["halo", "allgather"])
     args = ap.parse_args()
 
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -41,7 +42,8 @@ def main():
     import torch.distributed as dist
 
     import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200.sharded import LocalComm, ShardedJacobi, TorchDistComm, solve_duals_sharded
+    from paper_2011_08170_b200.sharded import (LocalComm, ShardedJacobi, TorchDistComm, make_halo_schedule,
+                                               solve_duals_sharded)
     from paper_2011_08170_b200 import _f2m
 
     f2m.set_device(local)
@@ -60,12 +62,19 @@ def main():
     line = {"n": args.n, "m": g.m, "world": comm.world, "clustered": args.clustered, "t_graph_s": t_graph}
     if args.solve:
         t0 = time.perf_counter()
-        lam, rep = solve_duals_sharded(g, comm, chunk=args.chunk, max_sweeps=200000)
+        lam, rep = solve_duals_sharded(g, comm, chunk=args.chunk, max_sweeps=200000, exchange=args.exchange)
         torch.cuda.synchronize()
         line.update(solve_s=time.perf_counter() - t0, sweeps=rep["sweeps"], converged=rep["converged"])
         if rank == 0:
             st, r1 = f2m.solve_duals(g, max_sweeps=200000)
             line.update(one_gpu_sweeps=r1["sweeps"], bit_identical=bool((lam == st.lam).all()))
+    elif args.exchange == "halo":
+        stream = torch.cuda.current_stream(dev)
+        sched, lam0, meta = make_halo_schedule(g, comm, chunk=args.chunk)
+        lam0s = [lam0] * len(meta["ranks"])
+        run = lambda k: sched.run(lam0s, -1.0, k)  # noqa: E731
+        run(max(args.warmup, 2 * args.chunk))
+        line["halo_values_per_sweep"] = meta["halo_values_per_sweep"]
     else:
         ranks = [comm.rank] if isinstance(comm, TorchDistComm) else list(range(comm.world))
         shards = [_f2m.shard_create(g, r, comm.world) for r in ranks]
@@ -80,13 +89,15 @@ def main():
 
         fns = [fn_of(sh) for sh in shards]
         sched = ShardedJacobi(fns, comm, stride, dev, args.chunk)
-        sched.run(lam0, -1.0, max(args.warmup, 2 * args.chunk))  # eager chunk + graph capture + replay
+        run = lambda k: sched.run(lam0, -1.0, k)  # noqa: E731
+        run(max(args.warmup, 2 * args.chunk))  # eager chunk + graph capture + replay
+    if not args.solve:
         torch.cuda.synchronize()
         if not args.local:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        sched.run(lam0, -1.0, args.sweeps)
+        run(args.sweeps)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -97,7 +108,8 @@ def main():
         per = ms * 1e3 / args.sweeps
         bytes_per_sweep = g.sweep_bytes()
         line.update(sweeps=args.sweeps, us_per_sweep=per, gdp_iterations_per_s=1e6 / per,
-                    algorithmic_GBps=bytes_per_sweep / (per * 1e-6) / 1e9, chunk=args.chunk)
+                    algorithmic_GBps=bytes_per_sweep / (per * 1e-6) / 1e9, chunk=args.chunk,
+                    exchange=args.exchange)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if not args.local:
