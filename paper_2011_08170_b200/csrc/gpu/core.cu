@@ -281,7 +281,7 @@ __global__ void k_window_apply(int n, const int32_t* __restrict__ old_of_new, co
 }
 
 
-// ---- CTA partition and CTA-local node order (sweep kernel v3)
+// ---- CTA partition and CTA-local node order (persistent sweep kernel)
 __global__ void k_slice_weight(int n, int64_t nslices, const int32_t* __restrict__ deg, int64_t* __restrict__ w) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= nslices) return;
@@ -444,7 +444,7 @@ __global__ void k_nbr_split(int64_t k, const uint64_t* __restrict__ keys, int32_
   atomicAdd(&cnt[keys[i] >> 32], 1);
 }
 
-// ---- v4 LL exchange: boundary publication indices
+// ---- LL exchange: boundary publication indices
 __global__ void k_boundary_counts(int ctas, int n, const int32_t* __restrict__ lo, const int32_t* __restrict__ nint,
                                   int32_t* __restrict__ cnt) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -620,7 +620,7 @@ static void build_local_index(Topology& t) {
     F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.nbr_off.get(), G + 1, s));
     launched("scan_nbr");
   }
-  // v4 LL publication indices (boundary nodes of each CTA, in position order)
+  // LL publication indices (boundary nodes of each CTA, in position order)
   t.boff.alloc(G + 1, s);
   t.halo_pub.alloc(std::max<int64_t>(h, 1), s);
   {
@@ -655,10 +655,11 @@ static void build_local_index(Topology& t) {
                                 (size_t)t.max_cta_slots * (sizeof(double) + sizeof(uint16_t)) + slice_bytes;
   const size_t streaming_bytes = lam_aligned + ids_bytes + slice_bytes;
   if (streaming_bytes > limit) return;  // v1 kernel
-  // The v3 kernel keeps per-sweep CTA maxima in a ring of 64. A CTA starts sweep s only after
-  // its own convergence helper has seen EVERY CTA publish sweep s-7, so no CTA runs more than
-  // ~16 sweeps ahead of any helper still reading the ring: 64 slots are race-free. The helper
-  // polls up to 256 CTAs per batch.
+  // The sweep kernel keeps per-sweep CTA maxima in a ring of kCmaxRing (64) slots. A CTA starts
+  // sweep s+1 only once the master has issued verdict s-7, and the master reads a window of 16
+  // sweeps from its next verdict on, so a slot is rewritten (sweep k+64) only long after the master
+  // has consumed it (window end <= verdict + 16 < k + 56): the ring is race-free for any G. The
+  // grid itself is one CTA per SM (G + master <= SM count); 256 bounds the partition tables.
   if (G > 256) return;  // v1 kernel
   t.v2 = true;
   t.resident = resident_bytes <= limit;

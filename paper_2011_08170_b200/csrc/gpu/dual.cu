@@ -295,112 +295,12 @@ __global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairs
   }
 }
 
-// ---------------------------------------------------------------- persistent Jacobi sweep v3
-// Neighbour-synchronised persistent kernel (no grid barrier).
-//  * CTA c owns a contiguous, degree-balanced slice range; inside it interior nodes (all
-//    neighbours in the CTA) come first, boundary nodes last.
-//  * lambda lives in four global buffers (sweep s reads glam[s%4], writes glam[(s+1)%4]) and,
-//    per CTA, in a shared-memory region [own | halo] (two regions, alternating, in resident
-//    mode, so the CTA's own multipliers never round-trip through L2).
-//  * The last warp is the sync warp: it waits until the CTAs owning this CTA's halo nodes
-//    have published sweep s-1 (per-CTA release flags), stages the halo multipliers into
-//    shared memory and signals named barrier 1, while the other 31 warps already update the
-//    interior slices. Boundary slices start after barrier 1.
-//  * Convergence (max|delta| <= eps*mean_cost, dual.cpp:235) of sweep k is evaluated by the
-//    sync warp during sweep k+3 from the CTAs' published maxima and applied at the top of
-//    sweep k+4 — before anything overwrites glam[(k+1)%4], the result of sweep k. All CTAs see
-//    the same maxima, so all stop at the same k; sweeps k+1..k+3 are discarded speculation.
-struct SweepCtl2 {
-  int error;
-  int sweeps;
-  int converged;
-  int out_buffer;
-  double final_max;
-};
-
-struct Sweep3Args {
-  int n;
-  const int64_t* __restrict__ sptr;
-  const int32_t* __restrict__ swidth;
-  const int32_t* __restrict__ cta_lo;
-  const int32_t* __restrict__ cta_int_hi;
-  const uint16_t* __restrict__ slidx;
-  const double* __restrict__ scost;
-  const int32_t* __restrict__ halo_off;
-  const int32_t* __restrict__ halo;
-  const int32_t* __restrict__ nbr_off;
-  const int32_t* __restrict__ nbr;
-  double* glam[8];  // lambda buffers: sweep s reads glam[s%8], writes glam[(s+1)%8]
-  int* flags;       // [G]: sweeps completed by CTA c
-  double* cmax;     // [kCmaxRing][G]: CTA max |delta| per sweep (ring)
-  double eta;
-  int update;
-  double threshold;
-  int max_sweeps;
-  double* record;
-  int lam_stride;  // doubles per shared-memory lambda region (16-byte multiple)
-  // optional phase trace (F2M_SWEEP_TRACE=first,count): globaltimer stamps per (sweep, CTA, phase)
-  unsigned long long* trace;
-  int trace_first, trace_count;
-};
-
-#define F2M_TRACE(S, PH)                                                                    \
-  do {                                                                                      \
-    if (a.trace && (S) >= a.trace_first && (S) < a.trace_first + a.trace_count)             \
-      a.trace[(((size_t)((S) - a.trace_first) * gridDim.x + blockIdx.x) << 3) + (PH)] =      \
-          globaltimer_ns();                                                                 \
-  } while (0)
-
 #define F2M_TRACE16(S, PH)                                                                  \
   do {                                                                                      \
     if (a.trace && (S) >= a.trace_first && (S) < a.trace_first + a.trace_count)             \
       a.trace[(((size_t)((S) - a.trace_first) * (G + 1) + blockIdx.x) << 4) + (PH)] =        \
           globaltimer_ns();                                                                 \
   } while (0)
-
-// one warp: wait until every CTA has published >= target. Loads are issued as a batch (the
-// reduction comes after all of them), so a poll costs one L2 round trip, not ceil(G/32).
-constexpr int kMaxCtaBatch = 8;  // supports G <= 256 CTAs
-__device__ __forceinline__ bool wait_all_ctas(const int* flags, int G, int target, int* err_local) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t t0 = globaltimer_ns();
-  for (;;) {
-    int v[kMaxCtaBatch];
-#pragma unroll
-    for (int b = 0; b < kMaxCtaBatch; ++b) {
-      const int i = lane + 32 * b;
-      v[b] = i < G ? ld_relaxed(flags + i) : INT_MAX;
-    }
-    int mn = INT_MAX;
-#pragma unroll
-    for (int b = 0; b < kMaxCtaBatch; ++b) mn = min(mn, v[b]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if (mn >= target) break;
-    if (globaltimer_ns() - t0 > 20ull * 1000000000ull) { *err_local = 1; return false; }
-  }
-  fence_acq_rel_gpu();
-  return true;
-}
-
-__device__ __forceinline__ double global_max(const double* v, int G) {
-  const int lane = threadIdx.x & 31;
-  double x[kMaxCtaBatch];
-#pragma unroll
-  for (int b = 0; b < kMaxCtaBatch; ++b) {
-    const int i = lane + 32 * b;
-    x[b] = i < G ? __ldcg(v + i) : 0.0;
-  }
-  double mx = 0.0;
-#pragma unroll
-  for (int b = 0; b < kMaxCtaBatch; ++b) mx = mx < x[b] ? x[b] : mx;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const double y = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = mx < y ? y : mx;
-  }
-  return mx;
-}
 
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -412,262 +312,23 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 constexpr int kLamBufs = 8;     // convergence verdicts may lag the sweeps by up to 7
 constexpr int kCmaxRing = 64;   // CTAs stay within ~16 sweeps of every helper (see core.cu)
 
-__device__ __forceinline__ int vload(const volatile int* p) { return *p; }
-
-template <int B, bool RES>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep3(Sweep3Args a, SweepCtl2* ctl) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[kSweepThreads / 32];
-  __shared__ unsigned long long wstart[kSweepThreads / 32], wfin[kSweepThreads / 32];
-  __shared__ int s_stop, s_err;
-  // helper -> main loop (volatile, no barrier between them)
-  __shared__ int h_done, h_conv, h_exit;
-  __shared__ double h_g, h_gconv;
-  const int c = blockIdx.x, G = gridDim.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int sync_warp = nwarps - 1, helper_warp = nwarps - 2, ncw = nwarps - 2;
-  const int main_threads = (nwarps - 1) * 32;  // all but the helper warp
-  const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
-  const int p0 = s_lo * 32;
-  const int own = max(0, min(s_hi * 32, a.n) - p0);
-  const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
-  const int nb0 = a.nbr_off[c], nnb = a.nbr_off[c + 1] - nb0;
-  const int64_t slot0 = a.sptr[s_lo];
-  const int nslots = (int)(a.sptr[s_hi] - slot0);
-  // shared memory: [lam A | lam B (resident)] [halo ids] [cost | local index (resident)]
-  double* regA = reinterpret_cast<double*>(smem);
-  double* regB = regA + (RES ? a.lam_stride : 0);
-  int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
-  double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
-  uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
-  const double* __restrict__ gcost = a.scost + slot0;
-  const uint16_t* __restrict__ glid = a.slidx + slot0;
-  for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo[h0 + i];
-  if (RES) {  // the CTA's slot data and own multipliers stay in shared memory for the whole solve
-    for (int i = tid; i < nslots; i += blockDim.x) {
-      cst_s[i] = gcost[i];
-      lid_s[i] = glid[i];
-    }
-    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.glam[0][p0 + i];
-  }
-  if (tid < kSweepThreads / 32) wstart[tid] = wfin[tid] = 0;
-  if (tid == 0) {
-    s_err = 0;
-    h_done = 0;
-    h_conv = -1;
-    h_exit = 0;
-    h_g = INFINITY;
-    h_gconv = INFINITY;
-  }
-  __syncthreads();
-
-  if (warp == helper_warp) {
-    // ---- convergence helper: verdict on sweep k once every CTA has published it
-    // (max|delta| <= eps*mean_cost, dual.cpp:235). Runs beside the sweeps, never in their way.
-    for (int k = 0; k < a.max_sweeps; ++k) {
-      const uint64_t t0 = globaltimer_ns();
-      bool ready = false;
-      while (!ready) {
-        int v[kMaxCtaBatch];
-#pragma unroll
-        for (int b = 0; b < kMaxCtaBatch; ++b) {
-          const int i = lane + 32 * b;
-          v[b] = i < G ? ld_relaxed(a.flags + i) : INT_MAX;
-        }
-        int mn = INT_MAX;
-#pragma unroll
-        for (int b = 0; b < kMaxCtaBatch; ++b) mn = min(mn, v[b]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        ready = mn >= k + 1;
-        if (!ready && (vload(&h_exit) || globaltimer_ns() - t0 > 20ull * 1000000000ull)) break;
-      }
-      if (!ready) {
-        if (!vload(&h_exit) && lane == 0) s_err = 1;
-        break;
-      }
-      fence_acq_rel_gpu();
-      const double g = global_max(a.cmax + (size_t)(k % kCmaxRing) * G, G);
-      if (lane == 0) {
-        if (c == 0 && a.record) a.record[k] = g;
-        h_g = g;
-        if (g <= a.threshold) {
-          h_gconv = g;
-          h_conv = k;
-        }
-        __threadfence_block();
-        h_done = k + 1;
-      }
-      __syncwarp();
-      if (g <= a.threshold) break;
-    }
-  } else {
-    // ---- main loop: 30 compute warps + the sync warp
-    for (int s = 0;; ++s) {
-      if (warp == 0 && lane == 0) {
-        int decided = -1;
-        // every verdict for k <= s - kLamBufs must be in before sweep s overwrites glam[(s+1)%8]
-        while (vload(&h_done) < s - kLamBufs + 1 && vload(&h_conv) < 0 && !vload(&s_err)) {
-        }
-        if (vload(&h_conv) >= 0) decided = vload(&h_conv);
-        else if (s >= a.max_sweeps) {
-          while (vload(&h_done) < a.max_sweeps && vload(&h_conv) < 0 && !vload(&s_err)) {
-          }
-          decided = vload(&h_conv) >= 0 ? vload(&h_conv) : a.max_sweeps - 1;
-        }
-        if (vload(&s_err)) decided = max(s - 1, 0);
-        s_stop = decided;
-      }
-      named_sync(2, main_threads);  // [A]
-      if (s_stop >= 0) break;
-      if (tid == 0) F2M_TRACE(s, 0);
-      double* lam = (RES && (s & 1)) ? regB : regA;
-      double* lam_next = (s & 1) ? regA : regB;
-      const double* gin = a.glam[s & 7];
-      double* gout = a.glam[(s + 1) & 7];
-      if (!RES) {  // stage own multipliers (written by this CTA last sweep)
-        for (int i = tid; i < own; i += main_threads) lam[i] = __ldcg(gin + p0 + i);
-        named_sync(2, main_threads);
-      }
-      double mx = 0.0;
-      if (warp == sync_warp) {
-        if (s >= 1) {  // halo owners have published sweep s-1 (or a verdict ended the solve)
-          const uint64_t t0 = globaltimer_ns();
-          for (;;) {
-            bool ok = true;
-            for (int i = lane; i < nnb; i += 32) ok &= ld_relaxed(a.flags + a.nbr[nb0 + i]) >= s;
-            if (__all_sync(0xffffffffu, ok)) break;
-            if (vload(&h_conv) >= 0) break;
-            if (globaltimer_ns() - t0 > 20ull * 1000000000ull) { s_err = 1; break; }
-          }
-          fence_acq_rel_gpu();
-        }
-        if (lane == 0) F2M_TRACE(s, 1);
-        for (int base = 0; base < nh; base += 32 * 8) {  // batched gathers: ~1 round trip
-          double v[8];
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            const int i = base + lane + 32 * b;
-            v[b] = i < nh ? __ldcg(gin + halo_s[i]) : 0.0;
-          }
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            const int i = base + lane + 32 * b;
-            if (i < nh) lam[own + i] = v[b];
-          }
-        }
-        __syncwarp();
-        if (lane == 0) F2M_TRACE(s, 2);
-        named_arrive(1, main_threads);  // arrive orders this warp's smem writes for bar.sync
-      } else {
-        bool halo_ready = false;
-        for (int sl = s_lo + warp; sl < s_hi; sl += ncw) {
-          if (!halo_ready && sl >= s_int) {
-            named_sync(1, main_threads);
-            halo_ready = true;
-            if (a.trace && lane == 0) wstart[warp] = globaltimer_ns();
-          }
-          const int p = sl * 32 + lane;
-          if (p >= a.n) continue;
-          const int lp = p - p0;
-          const int lb = (int)(a.sptr[sl] - slot0) + lane;
-          const int w = a.swidth[sl];
-          const double lv = lam[lp];
-          double sv[B + 1];
-#pragma unroll
-          for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-          int j = 0;
-          for (; j + 8 <= w; j += 8) {  // 8 slots in flight per thread
-            int li[8];
-            double cs[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int idx = lb + 32 * (j + u);
-              li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
-              cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
-          }
-          for (; j < w; ++j) {
-            const int idx = lb + 32 * j;
-            const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
-            const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
-            topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
-          }
-          const double d = delta_of<B>(sv, a.update);
-          const double nl = dadd(lv, dmul(a.eta, d));
-          gout[p] = nl;
-          if (RES) lam_next[lp] = nl;
-          const double ad = fabs(d);
-          mx = mx < ad ? ad : mx;
-        }
-        if (warp == 0 && lane == 0) F2M_TRACE(s, 4);
-        if (a.trace && lane == 0) wfin[warp] = globaltimer_ns();
-        if (!halo_ready) named_sync(1, main_threads);
-      }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, mx, off);
-        mx = mx < o ? o : mx;
-      }
-      if (lane == 0) red[warp] = mx;
-      named_sync(2, main_threads);  // [B]
-      if (tid == 0) F2M_TRACE(s, 5);
-      if (a.trace && tid == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count) {
-        unsigned long long bmin = ~0ULL, fmax = 0;
-        for (int w = 0; w < ncw; ++w) {
-          if (wstart[w] && wstart[w] < bmin) bmin = wstart[w];
-          if (wfin[w] > fmax) fmax = wfin[w];
-          wstart[w] = 0;
-        }
-        const size_t o = (((size_t)(s - a.trace_first) * gridDim.x + blockIdx.x) << 3);
-        a.trace[o + 3] = bmin == ~0ULL ? 0 : bmin;
-        a.trace[o + 7] = fmax;
-      }
-      if (warp == 0) {
-        double bm = (lane < nwarps && lane != helper_warp) ? red[lane] : 0.0;
-#pragma unroll
-        for (int off = 16; off; off >>= 1) {
-          const double o = __shfl_xor_sync(0xffffffffu, bm, off);
-          bm = bm < o ? o : bm;
-        }
-        if (lane == 0) {
-          a.cmax[(size_t)(s % kCmaxRing) * G + c] = bm;
-          // release (cumulative over the CTA's writes ordered before it by the barrier)
-          st_release(a.flags + c, s + 1);
-          F2M_TRACE(s, 6);
-        }
-      }
-    }
-    if (tid == 0) h_exit = 1;
-  }
-  __syncthreads();
-  if (tid == 0 && s_err) atomicExch(&ctl->error, 1);
-  if (c == 0 && tid == 0) {
-    const int k = s_stop;
-    ctl->sweeps = k + 1;
-    ctl->converged = h_conv >= 0 ? 1 : 0;
-    ctl->final_max = h_conv >= 0 ? h_gconv : h_g;
-    ctl->out_buffer = (k + 1) & 7;
-  }
-}
-
-// ---------------------------------------------------------------- persistent Jacobi sweep v4
-// v3's CTA-local structure (interior-first slices, smem-resident slots and multipliers, a sync
-// warp staging the halo while the other warps update interior nodes) with the inter-CTA traffic
-// moved to an LL ("low-latency") protocol: every published fp64 value travels as two 8-byte
-// words {tag:32 | half:32}, written with one relaxed 16-byte store and polled with one relaxed
-// 16-byte load. A word is single-copy atomic, so a matching tag in both words proves the value is
-// complete — no fences, no flags, one L2 trip from producer to consumer (tools/microbench:
-// LL round trip 0.5-1.1 us vs 1.4-2.6 us for release/acquire flags).
+// ---------------------------------------------------------------- persistent Jacobi sweep (LL)
+// Partition-resident persistent kernel with no grid barrier.
+//  * CTA c owns a contiguous, degree-balanced slice range; interior rows (all neighbours in the
+//    CTA) first, boundary rows last. In resident mode the CTA's slot costs / local indices and
+//    its multipliers live in shared memory for the whole solve (two lambda regions alternate).
+//  * Inter-CTA traffic uses an LL ("low-latency") protocol: every published fp64 value travels
+//    as two 8-byte words {tag:32 | half:32}, written with one relaxed 16-byte store and polled
+//    with one relaxed 16-byte load. A word is single-copy atomic, so a matching tag in both
+//    words proves the value is complete — no fences, no flags, one L2 trip from producer to
+//    consumer (tools/microbench/pingpong.cu: 0.5-1.1 us vs 1.4-2.6 us for release/acquire flags).
 //  * boundary node p of CTA c publishes lambda after sweep s at ll[(s+1)%kLLRing][boff[c] + p -
 //    p0 - nint[c]] with tag s+1; halo readers poll exactly those entries (halo_pub).
-//  * each CTA publishes its sweep max |delta| as an LL pair; CTA 0's master warp reduces them
+//  * each CTA publishes its sweep max |delta| as an LL pair; a dedicated master CTA reduces them
 //    in sweep order, applies max|delta| <= eps*mean_cost (dual.cpp:235) and publishes one
-//    control word {stop:32 | verdicts:32}. A CTA starts sweep s only once verdict s-8 exists, so
-//    the result of the stopping sweep k (glam[(k+1)%8]) is never overwritten; sweeps after k are
-//    speculation and are discarded.
+//    control word {stop:32 | verdicts:32}. A CTA starts sweep s+1 only once verdict s-7 exists,
+//    so the result of the stopping sweep k (ring buffer (k+1)%8) is never overwritten; sweeps
+//    after k are speculation and are discarded.
 constexpr int kLLRing = 4;
 
 __device__ __forceinline__ void st_ll(unsigned long long* p, double v, unsigned tag) {
@@ -747,329 +408,14 @@ struct Sweep4Args {
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
 
-template <int B, bool RES>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_gdp_sweep4(Sweep4Args a, Sweep4Ctl* ctl) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[kSweepThreads / 32];
-  __shared__ int s_stop;
-  __shared__ unsigned long long s_word;  // latest control word seen by the sync warp
-  const int c = blockIdx.x, G = gridDim.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int sync_warp = nwarps - 1, master_warp = nwarps - 2, ncw = nwarps - 2;
-  const int main_threads = (nwarps - 1) * 32;
-  const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
-  const int p0 = s_lo * 32;
-  const int own = max(0, min(s_hi * 32, a.n) - p0);
-  const int nint = a.cta_nint[c];
-  const int bo = a.boff[c] - nint;  // LL index of own local index lp >= nint is bo + lp
-  const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
-  const int64_t slot0 = a.sptr[s_lo];
-  const int nslots = (int)(a.sptr[s_hi] - slot0);
-  double* regA = reinterpret_cast<double*>(smem);
-  double* regB = regA + (RES ? a.lam_stride : 0);
-  int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
-  double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
-  uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
-  const double* __restrict__ gcost = a.scost + slot0;
-  const uint16_t* __restrict__ glid = a.slidx + slot0;
-  for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
-  if (RES) {
-    for (int i = tid; i < nslots; i += blockDim.x) {
-      cst_s[i] = gcost[i];
-      lid_s[i] = glid[i];
-    }
-    for (int i = tid; i < own; i += blockDim.x) regA[i] = a.gl[p0 + i];
-  }
-  if (tid == 0) {
-    s_word = 0ull;
-    s_stop = -1;
-  }
-  __syncthreads();
-
-  if (warp == master_warp) {
-    if (c != 0) return;  // only CTA 0 runs the convergence master
-    // ---- verdict on sweep k once every CTA has published its max |delta| for k
-    unsigned stop = 0;
-    double g = INFINITY;
-    int conv = 0;
-    for (int k = 0; k < a.max_sweeps && !stop; ++k) {
-      const unsigned tag = (unsigned)k + 1;
-      const unsigned long long* row = a.cmax + (size_t)(k % kCmaxRing) * G * 2;
-      double x[kMaxCtaBatch];
-      unsigned pend = 0;
-#pragma unroll
-      for (int b = 0; b < kMaxCtaBatch; ++b) {
-        x[b] = 0.0;
-        if (lane + 32 * b < G) pend |= 1u << b;
-      }
-      const uint64_t t0 = globaltimer_ns();
-      int it = 0;
-      while (__any_sync(0xffffffffu, pend != 0)) {
-        unsigned long long w0[kMaxCtaBatch], w1[kMaxCtaBatch];
-#pragma unroll
-        for (int b = 0; b < kMaxCtaBatch; ++b)
-          if (pend & (1u << b)) ld_ll_raw(row + 2 * (lane + 32 * b), w0[b], w1[b]);
-#pragma unroll
-        for (int b = 0; b < kMaxCtaBatch; ++b)
-          if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], tag)) {
-            x[b] = ll_val(w0[b], w1[b]);
-            pend &= ~(1u << b);
-          }
-        if ((++it & 63) == 0) {
-          int quit = 0;
-          if (lane == 0) {
-            quit = ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs;
-            if (quit) atomicExch(&ctl->abort, 1);
-          }
-          if (__shfl_sync(0xffffffffu, quit, 0)) {
-            stop = (unsigned)k;  // abandon: report what was decided so far
-            break;
-          }
-        }
-      }
-      if (__any_sync(0xffffffffu, pend != 0)) break;
-      double mx = 0.0;
-#pragma unroll
-      for (int b = 0; b < kMaxCtaBatch; ++b) mx = mx < x[b] ? x[b] : mx;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double y = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = mx < y ? y : mx;
-      }
-      g = mx;
-      if (g <= a.threshold) {
-        conv = 1;
-        stop = tag;
-      } else if (k == a.max_sweeps - 1) {
-        stop = tag;
-      }
-      if (lane == 0) {
-        if (a.record) a.record[k] = g;
-        st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | tag);
-      }
-    }
-    if (lane == 0) {
-      if (stop == 0) stop = 1;  // aborted before the first verdict
-      st_relaxed_u64(&ctl->word, ((unsigned long long)stop << 32) | stop);
-      ctl->sweeps = (int)stop;
-      ctl->converged = conv;
-      ctl->final_max = g;
-      ctl->out_buffer = (int)(stop & 7);
-    }
-    return;
-  }
-
-  // ---- main loop: ncw compute warps + the sync warp
-  for (int s = 0;; ++s) {
-    if (warp == 0 && lane == 0) {
-      // sweep s overwrites glam[(s+1)%8]: verdict s-8 must be in (or the solve must have stopped)
-      unsigned long long w = *(volatile unsigned long long*)&s_word;
-      const uint64_t t0 = globaltimer_ns();
-      int it = 0;
-      for (;;) {
-        const unsigned stop = (unsigned)(w >> 32), done = (unsigned)w;
-        if (stop) break;
-        if (s < a.max_sweeps && (int)done >= s - kLamBufs + 1) break;
-        if ((++it & 63) == 0 && (ld_relaxed(&ctl->abort) || globaltimer_ns() - t0 > kWatchdogNs)) {
-          atomicExch(&ctl->abort, 1);
-          w = (unsigned long long)(unsigned)max(s, 1) << 32;
-          break;
-        }
-        w = ld_relaxed_u64(&ctl->word);
-      }
-      s_stop = (w >> 32) ? (int)(w >> 32) - 1 : -1;
-    }
-    named_sync(2, main_threads);  // [A]
-    if (s_stop >= 0) break;
-    if (tid == 0) F2M_TRACE(s, 0);
-    double* lam = (RES && (s & 1)) ? regB : regA;
-    double* lam_next = (s & 1) ? regA : regB;
-    const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
-    double* gout = (a.gl + (size_t)((s + 1) & 7) * a.gstride);
-    if (!RES) {
-      for (int i = tid; i < own; i += main_threads) lam[i] = __ldcg(gin + p0 + i);
-      named_sync(2, main_threads);
-    }
-    double mx = 0.0;
-    if (warp == sync_warp) {
-      // ---- stage the halo of sweep s: LL entries with tag s (sweep 0: the initial multipliers)
-      const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
-      const uint64_t t0 = globaltimer_ns();
-      for (int base = 0; base < nh; base += 32 * 8) {
-        unsigned pend = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (base + lane + 32 * b < nh) pend |= 1u << b;
-        if (s == 0) {
-          double v[8];
-#pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (pend & (1u << b)) v[b] = __ldcg(gin + a.halo[h0 + base + lane + 32 * b]);
-#pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (pend & (1u << b)) lam[own + base + lane + 32 * b] = v[b];
-          continue;
-        }
-        int it = 0;
-        while (__any_sync(0xffffffffu, pend != 0)) {
-          unsigned long long w0[8], w1[8];
-#pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (pend & (1u << b)) ld_ll_raw(llin + 2 * halo_s[base + lane + 32 * b], w0[b], w1[b]);
-#pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], (unsigned)s)) {
-              lam[own + base + lane + 32 * b] = ll_val(w0[b], w1[b]);
-              pend &= ~(1u << b);
-            }
-          if (base == 0 && it == 0 && lane == 0) F2M_TRACE(s, 1);
-          if ((++it & 15) == 0) {
-            // a neighbour that stopped (verdict reached) never publishes again; a stalled one trips
-            // the watchdog. Either way this sweep's output is discarded.
-            int quit = 0;
-            if (lane == 0) {
-              const unsigned long long w = ld_relaxed_u64(&ctl->word);
-              s_word = w;
-              quit = (w >> 32) != 0 || ld_relaxed(&ctl->abort);
-              if (!quit && globaltimer_ns() - t0 > kWatchdogNs) {
-                atomicExch(&ctl->abort, 1);
-                quit = 1;
-              }
-            }
-            if (__shfl_sync(0xffffffffu, quit, 0)) {
-              pend = 0;
-              base = nh;
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) F2M_TRACE(s, 2);
-      named_arrive(1, main_threads);
-      if (lane == 0) s_word = ld_relaxed_u64(&ctl->word);  // off the critical path: for [A]
-    } else {
-      bool halo_ready = false;
-      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
-      for (int sl = s_lo + warp; sl < s_hi; sl += ncw) {
-        if (!halo_ready && sl >= s_int) {
-          named_sync(1, main_threads);
-          halo_ready = true;
-          if (lane == 0) F2M_TRACE(s, 3);
-        }
-        const int p = sl * 32 + lane;
-        if (p >= a.n) continue;
-        const int lp = p - p0;
-        const int lb = (int)(a.sptr[sl] - slot0) + lane;
-        const int w = a.swidth[sl];
-        const double lv = lam[lp];
-        double sv[B + 1];
-#pragma unroll
-        for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-        int j = 0;
-        for (; j + 8 <= w; j += 8) {
-          int li[8];
-          double cs[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int idx = lb + 32 * (j + u);
-            li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
-            cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
-        }
-        for (; j < w; ++j) {
-          const int idx = lb + 32 * j;
-          const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
-          const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
-          topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
-        }
-        const double d = delta_of<B>(sv, a.update);
-        const double nl = dadd(lv, dmul(a.eta, d));
-        if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);  // boundary: publish first
-        if (a.trace && halo_ready && lane == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count)
-          atomicMax(a.trace + ((((size_t)(s - a.trace_first) * gridDim.x + blockIdx.x) << 3) + 7), globaltimer_ns());
-        gout[p] = nl;
-        if (RES) lam_next[lp] = nl;
-        const double ad = fabs(d);
-        mx = mx < ad ? ad : mx;
-      }
-      if (warp == 0 && lane == 0) F2M_TRACE(s, 4);
-      if (!halo_ready) named_sync(1, main_threads);
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      const double o = __shfl_xor_sync(0xffffffffu, mx, off);
-      mx = mx < o ? o : mx;
-    }
-    if (lane == 0) red[warp] = mx;
-    named_sync(2, main_threads);  // [B]
-    if (tid == 0) F2M_TRACE(s, 5);
-    if (warp == 0) {
-      double bm = (lane < nwarps && lane != master_warp) ? red[lane] : 0.0;
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, bm, off);
-        bm = bm < o ? o : bm;
-      }
-      if (lane == 0) {
-        st_ll(a.cmax + ((size_t)(s % kCmaxRing) * G + c) * 2, bm, (unsigned)s + 1);
-        F2M_TRACE(s, 6);
-      }
-    }
-  }
-}
-
-template <int B, bool RES>
-static void launch_sweep4(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
-  auto fn = k_gdp_sweep4<B, RES>;
-  F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  void* args[] = {(void*)&a, (void*)&ctl};
-  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kSweepThreads), args, smem, s));
-}
-
-template <bool RES>
-static void dispatch_sweep4(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
-  switch (b) {
-    case 1: launch_sweep4<1, RES>(a, ctl, ctas, smem, s); break;
-    case 2: launch_sweep4<2, RES>(a, ctl, ctas, smem, s); break;
-    case 3: launch_sweep4<3, RES>(a, ctl, ctas, smem, s); break;
-    case 4: launch_sweep4<4, RES>(a, ctl, ctas, smem, s); break;
-    case 5: launch_sweep4<5, RES>(a, ctl, ctas, smem, s); break;
-    case 6: launch_sweep4<6, RES>(a, ctl, ctas, smem, s); break;
-    case 7: launch_sweep4<7, RES>(a, ctl, ctas, smem, s); break;
-    default: launch_sweep4<8, RES>(a, ctl, ctas, smem, s); break;
-  }
-}
-
-// ---------------------------------------------------------------- persistent Jacobi sweep v5
-// v4's LL exchange with the per-sweep critical path shortened:
+// Per-CTA roles (k_gdp_sweep5):
 //  * two sync warps run up to one sweep AHEAD of the compute warps: the halo of sweep s+1 is
 //    polled and staged into the idle shared-memory region while sweep s is still computing, and
-//    handed over through an mbarrier (no named barrier between the roles);
+//    handed over through named barriers (no CTA-wide barrier between the roles);
 //  * boundary rows (the only rows on the inter-CTA critical path) are computed by groups of L
 //    lanes (L = 1..8, as many as the CTA's boundary count allows) that split the row and merge
 //    their partial top-(B+1) lists with a bitonic merge, instead of one thread per row;
 //  * one CTA barrier per sweep: the stop decision for sweep s+1 is taken before barrier B of s.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
 
 // warp max of non-negative doubles (|delta|) through their bit patterns (monotone for x >= 0):
 // two REDUX ops instead of five 64-bit shuffle rounds. NaN is skipped like std::max(a, NaN) == a.
@@ -1629,28 +975,6 @@ size_t sweep_smem_limit(int dev) {
   return p.sharedMemPerBlockOptin > 8192 ? p.sharedMemPerBlockOptin - 8192 : 0;
 }
 
-template <int B, bool RES>
-static void launch_sweep2(const Sweep3Args& a, SweepCtl2* ctl, int ctas, size_t smem, cudaStream_t s) {
-  auto fn = k_gdp_sweep3<B, RES>;
-  F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  void* args[] = {(void*)&a, (void*)&ctl};
-  F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kSweepThreads), args, smem, s));
-}
-
-template <bool RES>
-static void dispatch_sweep2(int b, const Sweep3Args& a, SweepCtl2* ctl, int ctas, size_t smem, cudaStream_t s) {
-  switch (b) {
-    case 1: launch_sweep2<1, RES>(a, ctl, ctas, smem, s); break;
-    case 2: launch_sweep2<2, RES>(a, ctl, ctas, smem, s); break;
-    case 3: launch_sweep2<3, RES>(a, ctl, ctas, smem, s); break;
-    case 4: launch_sweep2<4, RES>(a, ctl, ctas, smem, s); break;
-    case 5: launch_sweep2<5, RES>(a, ctl, ctas, smem, s); break;
-    case 6: launch_sweep2<6, RES>(a, ctl, ctas, smem, s); break;
-    case 7: launch_sweep2<7, RES>(a, ctl, ctas, smem, s); break;
-    default: launch_sweep2<8, RES>(a, ctl, ctas, smem, s); break;
-  }
-}
-
 static double g_last_sweep_ms = 0.0;
 static std::string g_last_sweep_desc = "none";
 static int g_last_sweep_count = 0;
@@ -1662,17 +986,17 @@ static void launch_sweep(const SweepArgs& a, SweepCtl* ctl, int ctas, cudaStream
                                        args, 0, s));
 }
 
-// F2M_SWEEP_VARIANT=1|3|4|5 picks the sweep kernel for A/B measurements (default 5; 1 whenever the
-// per-CTA local index space does not fit). F2M_SWEEP_V1=1 is the older spelling of variant 1.
+// F2M_SWEEP_VARIANT=1 (or the older F2M_SWEEP_V1=1) forces the grid-barrier kernel for A/B
+// measurements; it is also used whenever the per-CTA local index space does not fit (!t.v2).
 static int g_variant = -1;
 
 static int sweep_variant(const Topology& t) {
   if (g_variant < 0) {
     g_variant = 5;
-    if (const char* e = std::getenv("F2M_SWEEP_VARIANT")) g_variant = std::atoi(e);
+    if (const char* e = std::getenv("F2M_SWEEP_VARIANT"))
+      if (std::atoi(e) == 1) g_variant = 1;
     if (const char* e = std::getenv("F2M_SWEEP_V1"))
       if (e[0] == '1') g_variant = 1;
-    if (g_variant != 1 && g_variant != 3 && g_variant != 4) g_variant = 5;
   }
   return t.v2 ? g_variant : 1;
 }
@@ -1686,7 +1010,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
   cudaStream_t s = t.stream;
   SweepResult r;
   if (max_sweeps <= 0) return r;
-  if (defer_eps > 0.0 && (g.mean_known || sweep_variant(t) != 5)) {
+  if (defer_eps > 0.0 && (g.mean_known || sweep_variant(t) == 1)) {
     threshold = defer_eps * graph_mean(g);  // host fp64 product, no FMA: == cfg.eps * mean_cost
     defer_eps = 0.0;
   }
@@ -1786,7 +1110,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     converged = h.converged;
     final_max = h.final_max;
     outbuf = (h.sweeps & 1) ? 1 : 0;
-  } else if (sweep_variant(t) >= 4) {
+  } else {
     const int G = t.sweep_ctas;
     DBuf<double> ring((size_t)kLamBufs * std::max(t.n, 1), s);
     DBuf<Sweep4Ctl> ctl(1, s);
@@ -1848,7 +1172,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       }
     }
     F2M_CUDA(cudaEventRecord(e0, s));
-    if (sweep_variant(t) == 5) {  // + 1 CTA: the convergence master
+    {  // + 1 CTA: the convergence master
       static int nt = -1;
       if (nt < 0) {
         const char* e = std::getenv("F2M_SWEEP_NT");
@@ -1865,11 +1189,6 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       else if (t.resident) dispatch_sweep5<true, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       else dispatch_sweep5<false, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       launched("gdp_sweep5");
-    } else {
-      g_last_sweep_desc = "k_gdp_sweep4<b=" + std::to_string(cfg.b) + "> (" + std::to_string(G) + " CTAs)";
-      if (t.resident) dispatch_sweep4<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
-      else dispatch_sweep4<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
-      launched("gdp_sweep4");
     }
     F2M_CUDA(cudaEventRecord(e1, s));
     Sweep4Ctl h;
@@ -1895,8 +1214,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       std::vector<unsigned long long> hbuf(trace.n);
       F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
       if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
-        const int hdr[4] = {a.trace_first, a.trace_count, -(sweep_variant(t) == 5 ? G + 1 : G),
-                            sweep_variant(t) == 5 ? 16 : 8};
+        const int hdr[4] = {a.trace_first, a.trace_count, -(G + 1), 16};
         std::fwrite(hdr, sizeof(int), 4, f);
         std::fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
         std::vector<int32_t> noff(G + 1);
@@ -1915,76 +1233,6 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
         std::fwrite(tmp.data(), sizeof(int32_t), G, f);
         F2M_CUDA(cudaMemcpy(tmp.data(), t.halo_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
         std::fwrite(tmp.data(), sizeof(int32_t), G + 1, f);
-        std::fclose(f);
-      }
-    }
-  } else {
-    const int G = t.sweep_ctas;
-    DBuf<double> extra((size_t)6 * std::max(t.n, 1), s);
-    DBuf<SweepCtl2> ctl(1, s);
-    DBuf<int> flags(G, s);
-    DBuf<double> cmax((size_t)kCmaxRing * G, s);
-    F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl2), s));
-    F2M_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * G, s));
-    Sweep3Args a;
-    a.n = t.n;
-    a.sptr = t.sptr.get();
-    a.swidth = t.swidth.get();
-    a.cta_lo = t.cta_lo.get();
-    a.cta_int_hi = t.cta_int_hi.get();
-    a.slidx = t.slidx.get();
-    a.scost = g.scost.get();
-    a.halo_off = t.halo_off.get();
-    a.halo = t.halo.get();
-    a.nbr_off = t.nbr_off.get();
-    a.nbr = t.nbr.get();
-    a.glam[0] = d_lam0;
-    a.glam[1] = d_lam1;
-    for (int i = 2; i < kLamBufs; ++i) a.glam[i] = extra.get() + (size_t)(i - 2) * std::max(t.n, 1);
-    a.flags = flags.get();
-    a.cmax = cmax.get();
-    a.eta = cfg.eta;
-    a.update = cfg.update;
-    a.threshold = threshold;
-    a.max_sweeps = max_sweeps;
-    a.record = d_record;
-    a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
-    a.trace = nullptr;
-    a.trace_first = a.trace_count = 0;
-    DBuf<unsigned long long> trace;
-    if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {  // "first,count" -> f2m_sweep_trace.bin
-      std::sscanf(tr, "%d,%d", &a.trace_first, &a.trace_count);
-      if (a.trace_count > 0) {
-        trace.alloc((size_t)a.trace_count * G * 8, s);
-        F2M_CUDA(cudaMemsetAsync(trace.get(), 0, trace.bytes(), s));
-        a.trace = trace.get();
-      }
-    }
-    F2M_CUDA(cudaEventRecord(e0, s));
-    g_last_sweep_desc = "k_gdp_sweep3<b=" + std::to_string(cfg.b) + "> (" + std::to_string(G) + " CTAs)";
-    if (t.resident) dispatch_sweep2<true>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
-    else dispatch_sweep2<false>(cfg.b, a, ctl.get(), G, t.smem_bytes, s);
-    launched("gdp_sweep3");
-    F2M_CUDA(cudaEventRecord(e1, s));
-    SweepCtl2 h;
-    F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaStreamSynchronize(s));
-    error = h.error;
-    sweeps = h.sweeps;
-    converged = h.converged;
-    final_max = h.final_max;
-    outbuf = h.out_buffer;
-    if (outbuf >= 2 && t.n > 0)  // hand the result back in one of the caller's two buffers
-      F2M_CUDA(cudaMemcpyAsync(d_lam1, a.glam[outbuf], sizeof(double) * t.n, cudaMemcpyDeviceToDevice, s));
-    if (outbuf >= 2) outbuf = 1;
-    F2M_CUDA(cudaStreamSynchronize(s));
-    if (a.trace) {
-      std::vector<unsigned long long> hbuf(trace.n);
-      F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
-      if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
-        const int hdr[3] = {a.trace_first, a.trace_count, G};
-        std::fwrite(hdr, sizeof(int), 3, f);
-        std::fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
         std::fclose(f);
       }
     }

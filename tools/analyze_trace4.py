@@ -1,4 +1,4 @@
-"""Summarise f2m_sweep_trace.bin written by the v4 sweep kernel (F2M_SWEEP_TRACE=first,count).
+"""Summarise f2m_sweep_trace.bin written by the persistent sweep kernel (F2M_SWEEP_TRACE=first,count).
 
 phases (globaltimer ns per sweep, CTA): 0 top (after barrier A) | 1 first halo poll returned |
 2 halo staged | 3 boundary compute starts | 4 warp 0 interior done | 5 after barrier B |

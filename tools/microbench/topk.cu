@@ -1,6 +1,6 @@
 // Throughput of the per-slot selection step of the GDP sweep (top-3 of (c - lv) - l over a row)
 // on a full SM (148 CTAs x 1024 threads, rows in shared memory), for three formulations:
-//   A  DSETP + selects bubble (k_gdp_sweep3/4 today)
+//   A  DSETP + selects bubble (k_gdp_sweep5 today)
 //   B  fmin/fmax bubble (DMNMX if the ISA has it)
 //   C  ordered-int64 keys: compare-exchange on integers
 // Prints ns per slot-per-SM (lower is better) and the SASS opcode the compiler chose.
