@@ -281,6 +281,12 @@ int f2m_graph_positions(const f2m_graph* g, int32_t* position);
 int f2m_gather_f64(const double* d_src, const int32_t* d_idx, double* d_dst, int64_t count, void* stream);
 int f2m_scatter_f64(const double* d_src, const int32_t* d_idx, double* d_dst, int64_t count, void* stream);
 int f2m_ids_to_positions(const f2m_graph* g, const double* d_ids, double* d_pos, void* stream);
+/* d_out[j] = left-to-right fp64 sum (from +0.0, round-to-nearest, no contraction) of
+ * d_v[j*seg_len, min((j+1)*seg_len, k)), bit-identical to a sequential loop but evaluated in
+ * parallel (csrc/gpu/seqsum.cu). seg_len <= 0 or >= k: one segment. Replaces the reference's
+ * single-threaded accumulations: objective (primal.cpp:226-230), dual-objective chunk sums
+ * (dual.cpp:96-109, parallel.cpp chunking) and mean_cost (graph.cpp:47-49). */
+int f2m_seq_sums(const double* d_v, int64_t k, int64_t seg_len, double* d_out, void* stream);
 
 /* ---- instrumentation (bench.py / tests) ----------------------------------------------- */
 /* Number of kernels this library launched since load (all entry points). */

@@ -176,33 +176,6 @@ __global__ void k_scost(int64_t slots, const int32_t* __restrict__ seid,
   scost[t] = e >= 0 ? cost[e] : CUDART_INF;
 }
 
-// Graph::from_edges mean (graph.cpp:47-49): a SEQUENTIAL fp64 sum in edge order. It sets the
-// convergence threshold eps*mean_cost, so it must be bit-exact: one block stages coalesced
-// tiles in shared memory and a single thread adds them in order.
-__global__ void __launch_bounds__(256) k_sequential_mean(int64_t m, const double* __restrict__ c,
-                                                         double* __restrict__ out) {
-  __shared__ double tile[2][1024];
-  double acc = 0.0;
-  const int64_t ntiles = (m + 1023) / 1024;
-  if (ntiles > 0) {
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) tile[0][i] = i < m ? c[i] : 0.0;
-  }
-  __syncthreads();
-  for (int64_t t = 0; t < ntiles; ++t) {
-    const int cur = t & 1;
-    if (t + 1 < ntiles) {  // prefetch the next tile while thread 0 sums this one
-      const int64_t base = (t + 1) * 1024;
-      for (int i = threadIdx.x; i < 1024; i += blockDim.x)
-        tile[cur ^ 1][i] = base + i < m ? c[base + i] : 0.0;
-    }
-    if (threadIdx.x == 0) {
-      const int cnt = (int)min64(1024, m - t * 1024);
-      for (int i = 0; i < cnt; ++i) acc = dadd(acc, tile[cur][i]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = m > 0 ? __ddiv_rn(acc, (double)m) : 0.0;
-}
 
 __global__ void k_jitter(int64_t m, const double* __restrict__ cin, double amplitude,
                          uint64_t state0, double* __restrict__ cout) {
@@ -787,14 +760,17 @@ void finalize_topology(Topology& t) {
   build_local_index(t);
 }
 
+// Graph::from_edges mean (graph.cpp:47-49): a SEQUENTIAL fp64 sum in edge order divided by m. It
+// sets the convergence threshold eps*mean_cost, so it must be bit-exact: seq_sums_device
+// reproduces the left-to-right chain; the division is IEEE (correctly rounded) on the host.
 double sequential_mean(const double* d_cost, int64_t m, cudaStream_t s) {
+  if (m <= 0) return 0.0;
   DBuf<double> out(1, s);
-  k_sequential_mean<<<1, 256, 0, s>>>(m, d_cost, out.get());
-  launched("sequential_mean");
+  seq_sums_device(d_cost, m, m, out.get(), s);
   double h = 0.0;
   F2M_CUDA(cudaMemcpyAsync(&h, out.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
-  return h;
+  return h / (double)m;
 }
 
 void attach_costs(f2m_graph& g) {

@@ -1383,50 +1383,22 @@ __global__ void k_node_delta(int p, int d, const int64_t* __restrict__ sptr,
 }
 
 // ---------------------------------------------------------------- dual objective
-__global__ void __launch_bounds__(256) k_dual_chunks(int n, int64_t m, int nchunks_node,
-                                                     int nchunks_edge, const int32_t* __restrict__ perm,
-                                                     const int32_t* __restrict__ eu,
-                                                     const int32_t* __restrict__ ev,
-                                                     const double* __restrict__ cost,
-                                                     const double* __restrict__ lam,
-                                                     double* __restrict__ parts) {
-  // one warp per chunk; the 32 lanes stage 256 terms of the chunk in shared memory, lane 0 adds
-  // them in order (the reference's per-chunk sequential sum, combined in chunk order later)
-  __shared__ double tile[8][256];
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int wl = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nchunks_node + nchunks_edge) return;
-  const bool node = w < nchunks_node;
-  const int64_t b = node ? (int64_t)w * kNodeChunk : (int64_t)(w - nchunks_node) * kEdgeChunk;
-  const int64_t e = node ? min64(n, b + kNodeChunk) : min64(m, b + kEdgeChunk);
-  double acc = 0.0;
-  for (int64_t base = b; base < e; base += 256) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t i = base + lane + 32 * k;
-      double v = 0.0;
-      if (i < e) {
-        if (node) {
-          v = lam[perm[i]];  // acc += lambda[v] (dual.cpp:96-100)
-        } else {
-          // if (v_e < 0) acc += v_e, v_e = (c - l_u) - l_v (dual.cpp:101-109). Adding +0.0 for the
-          // others is exact: acc is +0.0 or a negative non-zero sum, both unchanged by +0.0.
-          const double x = dsub(dsub(cost[i], lam[perm[eu[i]]]), lam[perm[ev[i]]]);
-          v = x < 0.0 ? x : 0.0;
-        }
-      }
-      tile[wl][lane + 32 * k] = v;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const int cnt = (int)min64(256, e - base);
-#pragma unroll 8
-      for (int k = 0; k < cnt; ++k) acc = dadd(acc, tile[wl][k]);
-    }
-    __syncwarp();
+// Terms of the dual objective in the reference's accumulation order: lambda[v] for the node
+// chunks (dual.cpp:96-100) and min(v_e, 0) for the edge chunks, v_e = (c - l_u) - l_v
+// (dual.cpp:101-109). Adding +0.0 for v_e >= 0 is exact: an edge chunk's running value is +0.0
+// or a negative non-zero sum, both unchanged by +0.0.
+__global__ void __launch_bounds__(256) k_dual_terms(int n, int64_t m, const int32_t* __restrict__ perm,
+                                                    const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                                                    const double* __restrict__ cost, const double* __restrict__ lam,
+                                                    double* __restrict__ terms) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    terms[i] = lam[perm[i]];
+  } else if (i < n + m) {
+    const int64_t e = i - n;
+    const double x = dsub(dsub(cost[e], lam[perm[eu[e]]]), lam[perm[ev[e]]]);
+    terms[i] = x < 0.0 ? x : 0.0;
   }
-  if (lane == 0) parts[w] = acc;
 }
 
 __global__ void k_dual_combine(int nchunks_node, int nchunks_edge, int b, const double* __restrict__ parts,
@@ -1445,9 +1417,13 @@ double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b)
   const int ne = (int)((t.m + kEdgeChunk - 1) / kEdgeChunk);
   DBuf<double> parts(nn + ne + 1, s);
   if (nn + ne > 0) {
-    k_dual_chunks<<<grid_for((int64_t)(nn + ne) * 32, 256), 256, 0, s>>>(
-        t.n, t.m, nn, ne, t.perm.get(), t.eu.get(), t.ev.get(), g.cost.get(), d_lam_pos, parts.get());
-    launched("dual_chunks");
+    // the reference's per-chunk sequential sums (parallel.cpp chunking), bit-exact (seqsum.cu)
+    DBuf<double> terms((size_t)t.n + t.m, s);
+    k_dual_terms<<<grid_for((int64_t)t.n + t.m, 256), 256, 0, s>>>(t.n, t.m, t.perm.get(), t.eu.get(), t.ev.get(),
+                                                                  g.cost.get(), d_lam_pos, terms.get());
+    launched("dual_terms");
+    if (t.n > 0) seq_sums_device(terms.get(), t.n, kNodeChunk, parts.get(), s);
+    if (t.m > 0) seq_sums_device(terms.get() + t.n, t.m, kEdgeChunk, parts.get() + nn, s);
   }
   k_dual_combine<<<1, 1, 0, s>>>(nn, ne, b, parts.get(), parts.get() + nn + ne);
   launched("dual_combine");

@@ -209,6 +209,9 @@ void identity_perm(Topology& t);
 // cost -> scost, mean_cost (bit-exact sequential sum on the device).
 void attach_costs(f2m_graph& g);
 double sequential_mean(const double* d_cost, int64_t m, cudaStream_t s);
+// out[j] = the left-to-right fp64 sum (from +0.0, __dadd_rn) of v[j*seg_len, min((j+1)*seg_len, k)),
+// bit-exact with a sequential loop, evaluated in parallel (seqsum.cu). seg_len <= 0: one segment.
+void seq_sums_device(const double* v, int64_t k, int64_t seg_len, double* out, cudaStream_t s);
 // The graph's mean_cost, computing it (sequential sum on the device) if still unknown.
 double graph_mean(const f2m_graph& g);
 

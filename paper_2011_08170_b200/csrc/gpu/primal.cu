@@ -10,9 +10,8 @@
 //  completion    one thread per component runs the reference's exhaustive DFS
 //                (solve_zero_component, primal.cpp:65-140) iteratively, same visiting order,
 //                same "first minimum wins" pruning -> identical x.
-//  objective     sequential fp64 sum in edge order (primal.cpp:226-230). Zero-valued edges
-//                contribute exactly +0, so the non-zero products are compacted (order kept)
-//                and one thread sums them: bit-exact with the reference.
+//  objective     sequential fp64 sum in edge order (primal.cpp:226-230), reproduced bit-exactly
+//                by the parallel exact-sequential-sum primitive (seqsum.cu).
 //  verify        per-node sums over the SELL rows (all partial sums are exact multiples of
 //                1/2), value-set check, gap = objective - g(lambda) (primal.cpp:235-276).
 #include <cub/cub.cuh>
@@ -225,37 +224,10 @@ __global__ void k_one_component(int mc, const int32_t* __restrict__ comp, const 
 }
 
 __global__ void k_products(int64_t m, const double* __restrict__ cost, const double* __restrict__ x,
-                           double* __restrict__ prod, uint8_t* __restrict__ nz) {
+                           double* __restrict__ prod) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
   prod[e] = dmul(cost[e], x[e]);
-  nz[e] = x[e] != 0.0;
-}
-
-// Sequential sum of v[0..k) (single block, tiles staged in shared memory).
-__global__ void __launch_bounds__(256) k_sequential_sum(const int64_t* __restrict__ kp,
-                                                        const double* __restrict__ v,
-                                                        double* __restrict__ out) {
-  __shared__ double tile[2][1024];
-  const int64_t k = *kp;
-  double acc = 0.0;
-  const int64_t ntiles = (k + 1023) / 1024;
-  if (ntiles > 0)
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) tile[0][i] = i < k ? v[i] : 0.0;
-  __syncthreads();
-  for (int64_t t = 0; t < ntiles; ++t) {
-    const int cur = t & 1;
-    if (t + 1 < ntiles) {
-      const int64_t base = (t + 1) * 1024;
-      for (int i = threadIdx.x; i < 1024; i += blockDim.x) tile[cur ^ 1][i] = base + i < k ? v[base + i] : 0.0;
-    }
-    if (threadIdx.x == 0) {
-      const int cnt = (int)min64(1024, k - t * 1024);
-      for (int i = 0; i < cnt; ++i) acc = dadd(acc, tile[cur][i]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = acc;
 }
 
 __global__ void k_node_sums(int n, const int32_t* __restrict__ perm, const int32_t* __restrict__ deg,
@@ -382,19 +354,10 @@ double objective_device(const f2m_graph& g, const double* d_x) {
   cudaStream_t s = t.stream;
   const int64_t m = t.m;
   if (m == 0) return 0.0;
-  DBuf<double> prod(m, s), nzv(m, s);
-  DBuf<uint8_t> nz(m, s);
-  k_products<<<grid_for(m, 256), 256, 0, s>>>(m, g.cost.get(), d_x, prod.get(), nz.get());
+  DBuf<double> prod(m, s), out(1, s);
+  k_products<<<grid_for(m, 256), 256, 0, s>>>(m, g.cost.get(), d_x, prod.get());
   launched("products");
-  DBuf<int64_t> nsel(1, s);
-  size_t tmp = 0;
-  F2M_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, prod.get(), nz.get(), nzv.get(), nsel.get(), m, s));
-  DBuf<char> tb(tmp, s);
-  F2M_CUDA(cub::DeviceSelect::Flagged(tb.get(), tmp, prod.get(), nz.get(), nzv.get(), nsel.get(), m, s));
-  launched("select_nonzero");
-  DBuf<double> out(1, s);
-  k_sequential_sum<<<1, 256, 0, s>>>(nsel.get(), nzv.get(), out.get());
-  launched("sequential_sum");
+  seq_sums_device(prod.get(), m, m, out.get(), s);  // the reference's left-to-right chain, exactly
   double h = 0.0;
   F2M_CUDA(cudaMemcpyAsync(&h, out.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));

@@ -480,6 +480,13 @@ PYBIND11_MODULE(_f2m, m) {
       },
       py::arg("src"), py::arg("idx"), py::arg("dst"), py::arg("count"), py::arg("stream") = 0);
   m.def(
+      "seq_sums",
+      [](std::uintptr_t v, std::int64_t k, std::int64_t seg_len, std::uintptr_t out, std::uintptr_t stream) {
+        f2m::check(f2m_seq_sums(reinterpret_cast<const double*>(v), k, seg_len, reinterpret_cast<double*>(out),
+                                reinterpret_cast<void*>(stream)));
+      },
+      py::arg("d_v"), py::arg("k"), py::arg("seg_len"), py::arg("d_out"), py::arg("stream") = 0);
+  m.def(
       "ids_to_positions",
       [](const f2m::Graph& graph, std::uintptr_t d_ids, std::uintptr_t d_pos, std::uintptr_t stream) {
         f2m::check(f2m_ids_to_positions(graph.handle(), reinterpret_cast<const double*>(d_ids),
