@@ -21,7 +21,8 @@
 //                    terms, terms >= 2^(E+1), or a zero / subnormal prediction;
 //   4. k_ss_super    kSuper consecutive chunks with the same prediction combine associatively;
 //   5. k_ss_walk     one CTA per segment walks the super-chunks in order with the EXACT running
-//                    value: a super-chunk (or, below it, a chunk) is applied in O(1) only if the
+//                    value (warp 0, 32 descriptors per round via a warp scan of their Q): a
+//                    super-chunk (or, below it, a chunk) is applied in O(1) only if the
 //                    exact value sits in the predicted binade with the predicted sign and every
 //                    partial sum a + P_i stays in [2^52 + 1, 2^53 - 1] ulps (so every exact
 //                    intermediate sum stays inside the binade); otherwise the chunk's terms are
@@ -37,7 +38,8 @@ namespace f2mgpu {
 
 namespace {
 
-constexpr int kChunk = 128;  // terms per chunk (4 per lane of the describing warp)
+constexpr int kChunk = 64;   // terms per chunk (kLaneTerms per lane of the describing warp)
+constexpr int kLaneTerms = kChunk / 32;
 constexpr int kSuper = 32;   // chunks per super-chunk
 constexpr int kWalkThreads = 256;
 constexpr long long kTwo52 = 1LL << 52;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(256) k_ss_approx(SegGeom g, int64_t nchunks, c
   g.chunk_range(c, lo, hi);
   double s = 0.0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < kLaneTerms; ++j) {
     const int64_t i = lo + lane + 32 * j;
     if (i < hi) s += v[i];
   }
@@ -135,11 +137,11 @@ __global__ void __launch_bounds__(256) k_ss_desc(SegGeom g, int64_t nchunks, con
   const int be = (int)((sb >> 52) & 0x7ff);
   const bool neg = (sb >> 63) != 0;
   bool ok = be != 0 && be != 0x7ff;  // zero / subnormal / non-finite prediction: walk it
-  // lane owns terms lo + 4*lane .. +3 (in order); local inclusive prefix, min / max
+  // lane owns kLaneTerms consecutive terms (in order); local inclusive prefix, min / max
   long long p = 0, lmn = LLONG_MAX, lmx = LLONG_MIN;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t i = lo + 4 * lane + j;
+  for (int j = 0; j < kLaneTerms; ++j) {
+    const int64_t i = lo + kLaneTerms * lane + j;
     if (i < hi) {
       long long q = 0;
       ok = quantise(v[i], be, neg, q) && ok;
@@ -211,18 +213,46 @@ __global__ void __launch_bounds__(256) k_ss_super(int64_t nsup_total, int64_t cp
   sdesc[t] = r;
 }
 
-// apply a descriptor to the exact running value if that is provably what the chain does
-__device__ __forceinline__ bool try_apply(double& acc, const SumDesc& d) {
-  if (d.flags & kEmpty) return true;
-  if (d.flags & kBad) return false;
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
-  const int be = (int)((bits >> 52) & 0x7ff);
-  if (be != d.be || (int)(bits >> 63) != ((d.flags & kNeg) ? 1 : 0)) return false;
-  const long long a = (long long)((bits & kMant) | (1ull << 52));
-  if (a + d.mn < kTwo52 + 1 || a + d.mx > 2 * kTwo52 - 1) return false;
-  const unsigned long long na = (unsigned long long)(a + d.q);
-  acc = __longlong_as_double((long long)((bits & ~kMant) | (na & kMant)));
-  return true;
+// Warp 0 advances the exact running value over descriptors D[i..cnt), 32 at a time: a
+// descriptor applies in O(1) iff it is not bad, the running value is normal with the predicted
+// binade and sign, and — given every earlier descriptor of the round applied (exclusive scan of
+// their Q) — all of its partial sums stay inside [2^52 + 1, 2^53 - 1] ulps (then every exact
+// intermediate sum is inside the binade and each add is acc + RNE_ulp(t)). Stops at the first
+// descriptor that does not apply (returned in i, not applied) or at cnt. acc is warp-uniform.
+__device__ __forceinline__ void warp_advance(const SumDesc* D, int cnt, int& i, double& acc) {
+  const int lane = threadIdx.x & 31;
+  while (i < cnt) {
+    const int idx = i + lane;
+    const bool have = idx < cnt;
+    SumDesc d;
+    if (have) d = D[idx];
+    else d = SumDesc{0, 0, 0, 0, kEmpty};
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
+    const int be = (int)((bits >> 52) & 0x7ff);
+    const int sg = (int)(bits >> 63);
+    const bool normal = be != 0 && be != 0x7ff;
+    const long long a = (long long)((bits & kMant) | (1ull << 52));
+    const bool empty = (d.flags & kEmpty) != 0;
+    bool ok = empty || (!(d.flags & kBad) && normal && d.be == be && ((d.flags & kNeg) ? 1 : 0) == sg);
+    const long long q = (ok && !empty) ? d.q : 0;
+    long long incl = q;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const long long excl = incl - q;
+    if (ok && !empty) ok = a + excl + d.mn >= kTwo52 + 1 && a + excl + d.mx <= 2 * kTwo52 - 1;
+    const unsigned fail = __ballot_sync(0xffffffffu, have && !ok);
+    const int f = fail ? __ffs(fail) - 1 : min(32, cnt - i);
+    const long long add = f < 32 ? __shfl_sync(0xffffffffu, excl, f) : __shfl_sync(0xffffffffu, incl, 31);
+    if (normal && add != 0) {
+      const unsigned long long na = (unsigned long long)(a + add);
+      acc = __longlong_as_double((long long)((bits & ~kMant) | (na & kMant)));
+    }
+    i += f;
+    if (fail) return;
+  }
 }
 
 __global__ void __launch_bounds__(kWalkThreads) k_ss_walk(SegGeom g, const double* __restrict__ v,
@@ -231,12 +261,14 @@ __global__ void __launch_bounds__(kWalkThreads) k_ss_walk(SegGeom g, const doubl
                                                           double* __restrict__ out) {
   __shared__ SumDesc s_sup[kWalkThreads];
   __shared__ SumDesc s_ch[kSuper];
-  __shared__ double s_terms[kChunk];
+  __shared__ double s_terms[kSuper * kChunk];  // every term of the super-chunk being descended
   __shared__ int s_idx;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool walker = tid < 32;  // warp 0 holds the exact running value
   const int64_t seg = blockIdx.x;
   const int64_t sup0 = seg * g.sps, ch0 = seg * g.cps;
-  double acc = 0.0;  // exact running value (thread 0)
+  const int64_t seg_lo = seg * g.seg_len;
+  double acc = 0.0;
   for (int64_t sb = 0; sb < g.sps; sb += kWalkThreads) {
     const int nb = (int)min64(kWalkThreads, g.sps - sb);
     __syncthreads();
@@ -244,39 +276,48 @@ __global__ void __launch_bounds__(kWalkThreads) k_ss_walk(SegGeom g, const doubl
     __syncthreads();
     int j = 0;
     for (;;) {
-      if (tid == 0) {
-        while (j < nb && try_apply(acc, s_sup[j])) ++j;
-        s_idx = j;
+      if (walker) {
+        warp_advance(s_sup, nb, j, acc);
+        if (lane == 0) s_idx = j;
       }
       __syncthreads();
       j = s_idx;
       if (j >= nb) break;
-      // descend into super-chunk sb + j
+      // descend into super-chunk sb + j: stage its chunk descriptors and all of its terms in one
+      // round trip, then warp 0 walks the chunks, adding the terms of failing chunks in order
       const int64_t cfirst = ch0 + (sb + j) * kSuper;
       const int gc = (int)min64(kSuper, ch0 + g.cps - cfirst);
+      const int64_t tlo = min64(seg_lo + (cfirst - ch0) * kChunk, g.k);
+      const int64_t thi = min64(min64(tlo + (int64_t)gc * kChunk, seg_lo + g.seg_len), g.k);
       if (tid < gc) s_ch[tid] = desc[cfirst + tid];
+      {  // all loads in flight at once: one memory round trip per descent
+        constexpr int kPer = kSuper * kChunk / kWalkThreads;
+        const int cnt = (int)(thi - tlo);
+        double r[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int i = tid + u * kWalkThreads;
+          r[u] = i < cnt ? __ldg(v + tlo + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) s_terms[tid + u * kWalkThreads] = r[u];
+      }
       __syncthreads();
-      int i = 0;
-      for (;;) {
-        if (tid == 0) {
-          while (i < gc && try_apply(acc, s_ch[i])) ++i;
-          s_idx = i;
+      if (walker) {
+        int i = 0;
+        for (;;) {
+          warp_advance(s_ch, gc, i, acc);
+          if (i >= gc) break;
+          if (lane == 0) {
+            const int lo = i * kChunk, hi = (int)min64((int64_t)lo + kChunk, thi - tlo);
+            for (int t = lo; t < hi; ++t) acc = dadd(acc, s_terms[t]);
+          }
+          acc = __shfl_sync(0xffffffffu, acc, 0);
+          ++i;
         }
-        __syncthreads();
-        i = s_idx;
-        if (i >= gc) break;
-        int64_t lo, hi;
-        g.chunk_range(cfirst + i, lo, hi);
-        if (tid < hi - lo) s_terms[tid] = v[lo + tid];
-        __syncthreads();
-        if (tid == 0) {
-          const int cnt = (int)(hi - lo);
-          for (int t = 0; t < cnt; ++t) acc = dadd(acc, s_terms[t]);
-        }
-        ++i;
-        __syncthreads();
       }
       ++j;
+      __syncthreads();
     }
   }
   if (tid == 0) out[seg] = acc;
@@ -285,7 +326,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_ss_walk(SegGeom g, const doubl
 }  // namespace
 
 void seq_sums_device(const double* v, int64_t k, int64_t seg_len, double* out, cudaStream_t s) {
-  static_assert(kWalkThreads >= kChunk && kWalkThreads >= kSuper, "walk CTA stages a chunk / super");
+  static_assert(kWalkThreads >= kSuper && (kSuper * kChunk) % kWalkThreads == 0, "walk CTA stages a super-chunk");
   if (k <= 0) return;
   if (seg_len <= 0 || seg_len > k) seg_len = k;
   const int64_t nseg = (k + seg_len - 1) / seg_len;

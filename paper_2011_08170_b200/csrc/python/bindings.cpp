@@ -357,14 +357,27 @@ PYBIND11_MODULE(_f2m, m) {
   m.def(
       "full_solve_arrays",
       [](py::array_t<double, py::array::c_style | py::array::forcecast> xy, bool rounded, int k, double eps,
-         int max_sweeps, std::uint64_t seed, int max_restarts, double tol) {
+         int max_sweeps, std::uint64_t seed, int max_restarts, double tol, py::object out_value,
+         py::object out_duals) {
         const int n = static_cast<int>(xy.size() / 2);
         const int per = std::max(3, std::min(k, n - 1));
         f2m_run_config rc = run_config_c(k, 0.5, eps, max_sweeps, "jacobi", tol, max_restarts, seed, 1e-6, 1e-7);
-        // results land directly in (uninitialised) numpy buffers: m <= n * per (each node adds at
-        // most `per` candidate edges), the edge-value view is trimmed to m afterwards (no copy)
-        py::array_t<double> x(static_cast<py::ssize_t>(n) * per + 1);
-        py::array_t<double> lam(static_cast<py::ssize_t>(std::max(n, 1)));
+        // results land directly in numpy buffers: m <= n * per (each node adds at most `per`
+        // candidate edges), the edge-value view is trimmed to m afterwards (no copy). Callers that
+        // solve repeatedly pass their own (ideally page-locked) buffers: the device->host copies
+        // then run at DMA speed instead of faulting in fresh pageable pages every call.
+        const py::ssize_t xcap = static_cast<py::ssize_t>(n) * per + 1;
+        auto out_buffer = [](py::object o, py::ssize_t need, const char* what) {
+          py::array_t<double> a;
+          if (o.is_none()) return py::array_t<double>(need);
+          a = py::array_t<double>::ensure(o);
+          if (!a || !(a.flags() & py::array::c_style) || !a.writeable() || a.size() < need || !o.is(a))
+            throw py::value_error(std::string(what) + ": expected a writable C-contiguous float64 array of at least " +
+                                  std::to_string(need) + " elements");
+          return a;
+        };
+        py::array_t<double> x = out_buffer(out_value, xcap, "out_value");
+        py::array_t<double> lam = out_buffer(out_duals, std::max<py::ssize_t>(n, 1), "out_duals");
         double* px = x.mutable_data();
         double* pl = lam.mutable_data();
         f2m_solve_outcome o{};
@@ -384,7 +397,8 @@ PYBIND11_MODULE(_f2m, m) {
         return d;
       },
       py::arg("xy"), py::arg("rounded") = false, py::arg("k") = 10, py::arg("eps") = 1e-9,
-      py::arg("max_sweeps") = 20000, py::arg("seed") = 0, py::arg("max_restarts") = 5, py::arg("tol") = 0.0);
+      py::arg("max_sweeps") = 20000, py::arg("seed") = 0, py::arg("max_restarts") = 5, py::arg("tol") = 0.0,
+      py::arg("out_value") = py::none(), py::arg("out_duals") = py::none());
   m.def(
       "full_solve_device",
       [](int n, std::uintptr_t d_xy, bool rounded, int k, double eps, int max_sweeps, std::uintptr_t d_x,

@@ -59,6 +59,20 @@ def test_full_solve_arrays_c_abi(f2m):
     assert sha(r["duals"]) == meta["sha256"]["lam_full"]
 
 
+def test_full_solve_arrays_caller_buffers(f2m):
+    """Caller-owned (page-locked) result buffers: same bits, written in place, reused."""
+    import torch
+    inst, g, meta, _ = _graph(f2m, "u1k_s1")
+    xb = torch.full((1000 * 10 + 1,), -1.0, dtype=torch.float64).pin_memory().numpy()
+    lb = torch.full((1000,), -1.0, dtype=torch.float64).pin_memory().numpy()
+    for _ in range(2):
+        r = f2m.full_solve_arrays(inst.points_array(), k=10, out_value=xb, out_duals=lb)
+        assert r["objective"] == meta["full_objective"]
+        assert sha(r["value"]) == meta["sha256"]["x_full"]
+        assert sha(r["duals"]) == meta["sha256"]["lam_full"]
+        assert np.shares_memory(r["value"], xb) and np.shares_memory(r["duals"], lb)
+
+
 def _sq(f2m):
     return f2m.Instance.from_points(np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float))
 

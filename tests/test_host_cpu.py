@@ -100,6 +100,18 @@ def test_no_silent_cpu_fallback(f2m):
         f2m.full_solve(inst, k=5)
 
 
+def test_full_solve_arrays_rejects_bad_output_buffers(f2m):
+    """Caller-owned result buffers are checked before any device work (size, dtype, layout)."""
+    import numpy as np
+    xy = f2m.generate_instance(50, 1).points_array()
+    with pytest.raises(ValueError, match="out_value"):
+        f2m.full_solve_arrays(xy, k=5, out_value=np.zeros(10))
+    with pytest.raises(ValueError, match="out_value"):
+        f2m.full_solve_arrays(xy, k=5, out_value=np.zeros(251, dtype=np.float32))
+    with pytest.raises(ValueError, match="out_duals"):
+        f2m.full_solve_arrays(xy, k=5, out_value=np.zeros(251), out_duals=np.zeros(100)[::2])
+
+
 def _declared_symbols():
     text = open(os.path.join(ROOT, "include", "f2m_gpu.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
