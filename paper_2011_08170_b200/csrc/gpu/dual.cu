@@ -14,10 +14,11 @@
 //  k_init_local_midpoint  make_initial_state (dual.cpp:194-208) is an in-order Gauss-Seidel
 //                   pass from zero: node v sees the FINAL multipliers of lower-numbered
 //                   neighbours. Sync-free DAG execution: warps claim nodes in id order from a
-//                   global counter and spin on per-node done flags of lower neighbours.
+//                   global counter and poll the LL-published multipliers of lower neighbours.
 //  k_gs_sweep       gauss_seidel_sweep (dual.cpp:175-192): one warp, nodes in id order.
-//  k_dual_chunks    dual_objective (dual.cpp:87-123) in the reference's 2048/8192 chunk
-//                   order: one warp per chunk, lane 0 adds in sequence -> bit-exact.
+//  k_dual_terms     dual_objective (dual.cpp:87-123): the terms in the reference's order; the
+//                   2048/8192-chunk sequential sums come from seq_sums_device (seqsum.cu),
+//                   bit-exact.
 #include <chrono>
 #include <climits>
 #include <cstdlib>
@@ -1256,8 +1257,11 @@ template <int B>
 __global__ void __launch_bounds__(256) k_init_local_midpoint(
     int n, const int32_t* __restrict__ perm, const int32_t* __restrict__ iperm,
     const int32_t* __restrict__ deg, const int64_t* __restrict__ sptr,
-    const int32_t* __restrict__ scol, const double* __restrict__ scost, double* lam, int* done,
-    int* counter, int* err) {
+    const int32_t* __restrict__ scol, const double* __restrict__ scost, double* lam,
+    unsigned long long* ll, int* counter, int* err) {
+  // node p's final multiplier is published once as an LL pair {1:32 | half:32} x 2 (see st_ll):
+  // a reader's single 16-byte poll both detects completion and returns the value (no flag, no
+  // fence, one L2 round trip)
   const int lane = threadIdx.x & 31;
   for (;;) {
     int v = 0;
@@ -1276,32 +1280,37 @@ __global__ void __launch_bounds__(256) k_init_local_midpoint(
       double other = 0.0;  // lambda of a higher-numbered (or the same) node is still 0
       if (iperm[q] < v) {
         const uint64_t t0 = globaltimer_ns();
-        while (ld_relaxed(done + q) == 0) {
-          if (globaltimer_ns() - t0 > 20ull * 1000000000ull) { atomicExch(err, 1); break; }
+        unsigned long long w0, w1;
+        for (;;) {
+          ld_ll_raw(ll + 2 * (int64_t)q, w0, w1);
+          if (ll_ok(w0, w1, 1u)) break;
+          if (globaltimer_ns() - t0 > 20ull * 1000000000ull) {
+            atomicExch(err, 1);
+            break;
+          }
         }
-        fence_acq_rel_gpu();
-        other = __ldcg(lam + q);
+        other = ll_val(w0, w1);
       }
       // ge.cost - lv - other with lv = lambda[v] = 0 (dual.cpp:43)
       topk_insert<B>(s, dsub(dsub(c, 0.0), other));
     }
     warp_topk_merge<B>(s);
     if (lane == 0) {
-      lam[p] = d > B ? dmul(0.5, dadd(s[B - 1], s[B])) : 0.0;
-      __threadfence();
-      st_release(done + p, 1);
+      const double val = d > B ? dmul(0.5, dadd(s[B - 1], s[B])) : 0.0;
+      st_ll(ll + 2 * (int64_t)p, val, 1u);
+      lam[p] = val;
     }
   }
 }
 
 template <int B>
-static void launch_init(const f2m_graph& g, double* d_lam, int* done, int* counter, int* err) {
+static void launch_init(const f2m_graph& g, double* d_lam, unsigned long long* ll, int* counter, int* err) {
   const Topology& t = *g.topo;
   const int blocks = std::max(1, std::min<int>(grid_for((int64_t)t.n * 32, 256),
                                                device_props(t.dev).multiProcessorCount * 8));
   k_init_local_midpoint<B><<<blocks, 256, 0, t.stream>>>(t.n, t.perm.get(), t.iperm.get(), t.deg.get(),
                                                         t.sptr.get(), t.scol.get(), g.scost.get(), d_lam,
-                                                        done, counter, err);
+                                                        ll, counter, err);
   launched("init_local_midpoint");
 }
 
@@ -1311,20 +1320,22 @@ void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, doub
   if (t.n == 0) return;
   F2M_CUDA(cudaMemsetAsync(d_lam_pos, 0, sizeof(double) * t.n, s));
   if (cfg.init != 0) return;  // kZero
-  DBuf<int> flags(t.n + 2, s);
-  F2M_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * (t.n + 2), s));
-  int* done = flags.get();
-  int* counter = flags.get() + t.n;
-  int* err = flags.get() + t.n + 1;
+  DBuf<unsigned long long> ll((size_t)2 * t.n, s);
+  DBuf<int> flags(2, s);
+  F2M_CUDA(cudaMemsetAsync(ll.get(), 0, ll.bytes(), s));
+  F2M_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * 2, s));
+  unsigned long long* llp = ll.get();
+  int* counter = flags.get();
+  int* err = flags.get() + 1;
   switch (cfg.b) {
-    case 1: launch_init<1>(g, d_lam_pos, done, counter, err); break;
-    case 2: launch_init<2>(g, d_lam_pos, done, counter, err); break;
-    case 3: launch_init<3>(g, d_lam_pos, done, counter, err); break;
-    case 4: launch_init<4>(g, d_lam_pos, done, counter, err); break;
-    case 5: launch_init<5>(g, d_lam_pos, done, counter, err); break;
-    case 6: launch_init<6>(g, d_lam_pos, done, counter, err); break;
-    case 7: launch_init<7>(g, d_lam_pos, done, counter, err); break;
-    default: launch_init<8>(g, d_lam_pos, done, counter, err); break;
+    case 1: launch_init<1>(g, d_lam_pos, llp, counter, err); break;
+    case 2: launch_init<2>(g, d_lam_pos, llp, counter, err); break;
+    case 3: launch_init<3>(g, d_lam_pos, llp, counter, err); break;
+    case 4: launch_init<4>(g, d_lam_pos, llp, counter, err); break;
+    case 5: launch_init<5>(g, d_lam_pos, llp, counter, err); break;
+    case 6: launch_init<6>(g, d_lam_pos, llp, counter, err); break;
+    case 7: launch_init<7>(g, d_lam_pos, llp, counter, err); break;
+    default: launch_init<8>(g, d_lam_pos, llp, counter, err); break;
   }
   int herr = 0;
   F2M_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));

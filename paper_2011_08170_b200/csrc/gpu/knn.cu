@@ -132,14 +132,18 @@ __global__ void __launch_bounds__(128) k_knn_query(int n, int per_node, int roun
                                                    double* __restrict__ scratch_d,
                                                    int* __restrict__ scratch_i,
                                                    int32_t* __restrict__ nbr) {
-  const int node = blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= n) return;
+  // queries run in cell order (ids / pts are the points sorted by grid cell): the lanes of a warp
+  // scan overlapping neighbourhoods (L1 reuse, similar trip counts); results go to the node's row
+  const int tq = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tq >= n) return;
+  const int node = ids[tq];
   const GridParams p = *gpp;
   Best<KMAX> local;
   double* hd = KMAX > 0 ? local.d : scratch_d + (int64_t)node * per_node;
   int* hi = KMAX > 0 ? local.id : scratch_i + (int64_t)node * per_node;
   int cnt = 0;
-  const double ax = xy[2 * node], ay = xy[2 * node + 1];
+  const double2 self = pts[tq];
+  const double ax = self.x, ay = self.y;
   const int ccx = clamp_c(ax, p.min_x, p.cell, p.gx);
   const int ccy = clamp_c(ay, p.min_y, p.cell, p.gy);
   for (int r = 0; r <= p.max_ring; ++r) {
@@ -183,6 +187,77 @@ __global__ void __launch_bounds__(128) k_knn_query(int n, int per_node, int roun
     }
   }
   for (int j = 0; j < per_node; ++j) nbr[(int64_t)node * per_node + j] = hi[j];
+}
+
+// Fixed-K variant (K = per_node known at compile time): the sorted top-K list lives in
+// registers (fully unrolled insertion, no local memory). Same candidates, same (distance, id)
+// total order and the same ring-termination bound as k_knn_query -> identical lists.
+template <int K>
+__global__ void __launch_bounds__(128) k_knn_query_reg(int n, int rounded, const GridParams* __restrict__ gpp,
+                                                       const int32_t* __restrict__ off,
+                                                       const int32_t* __restrict__ ids,
+                                                       const double2* __restrict__ pts,
+                                                       int32_t* __restrict__ nbr) {
+  const int tq = blockIdx.x * blockDim.x + threadIdx.x;  // cell order (see k_knn_query)
+  if (tq >= n) return;
+  const int node = ids[tq];
+  const GridParams p = *gpp;
+  double hd[K];
+  int hi[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    hd[j] = CUDART_INF;
+    hi[j] = INT_MAX;
+  }
+  const double2 self = pts[tq];
+  const double ax = self.x, ay = self.y;
+  const int ccx = clamp_c(ax, p.min_x, p.cell, p.gx);
+  const int ccy = clamp_c(ay, p.min_y, p.cell, p.gy);
+  auto visit = [&](int cx, int cy) {
+    const int c = cy * p.gx + cx;
+    const int t1 = off[c + 1];
+    for (int t = off[c]; t < t1; ++t) {
+      const int q = ids[t];
+      if (q == node) continue;
+      const double2 b = pts[t];
+      const double dd = point_distance(ax, ay, b.x, b.y, rounded);
+      if (!(dd < hd[K - 1] || (dd == hd[K - 1] && q < hi[K - 1]))) continue;
+      bool placed = false;
+#pragma unroll
+      for (int j = K - 1; j > 0; --j) {
+        const bool lt = dd < hd[j - 1] || (dd == hd[j - 1] && q < hi[j - 1]);
+        const double nd = lt ? hd[j - 1] : (placed ? hd[j] : dd);
+        const int ni = lt ? hi[j - 1] : (placed ? hi[j] : q);
+        hd[j] = nd;
+        hi[j] = ni;
+        placed = placed || !lt;
+      }
+      if (!placed) {
+        hd[0] = dd;
+        hi[0] = q;
+      }
+    }
+  };
+  for (int r = 0; r <= p.max_ring; ++r) {
+    const int x0 = ccx - r, x1 = ccx + r, y0 = ccy - r, y1 = ccy + r;
+    const int ylo = max(0, y0), yhi = min(p.gy - 1, y1);
+    const int xlo = max(0, x0), xhi = min(p.gx - 1, x1);
+    for (int cy = ylo; cy <= yhi; ++cy) {
+      if (cy == y0 || cy == y1) {  // ring cells only (graph.cpp:212-214)
+        for (int cx = xlo; cx <= xhi; ++cx) visit(cx, cy);
+      } else {
+        if (x0 >= 0) visit(x0, cy);
+        if (x1 <= p.gx - 1) visit(x1, cy);
+      }
+    }
+    if (hi[K - 1] != INT_MAX) {  // K found; unseen points are at distance >= r*cell (graph.cpp:203-211)
+      double bound = dmul(dmul((double)r, p.cell), 1.0 - 1e-12);
+      if (rounded) bound = dsub(bound, 0.5);
+      if (bound > hd[K - 1]) break;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) nbr[(int64_t)node * K + j] = hi[j];
 }
 
 __global__ void k_pair_keys(int n, int per_node, const int32_t* __restrict__ nbr,
@@ -296,7 +371,14 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   DBuf<double> sd;
   DBuf<int> si;
   const unsigned qg = grid_for(n, 128);
-  if (per_node <= 16) {
+  if (per_node >= 3 && per_node <= 12) {
+    switch (per_node) {
+#define F2M_KQ(K) \
+  case K: k_knn_query_reg<K><<<qg, 128, 0, s>>>(n, rounded, gp.get(), off.get(), ids.get(), pts.get(), nbr.get()); break;
+      F2M_KQ(3) F2M_KQ(4) F2M_KQ(5) F2M_KQ(6) F2M_KQ(7) F2M_KQ(8) F2M_KQ(9) F2M_KQ(10) F2M_KQ(11) F2M_KQ(12)
+#undef F2M_KQ
+    }
+  } else if (per_node <= 16) {
     k_knn_query<16><<<qg, 128, 0, s>>>(n, per_node, rounded, d_xy, gp.get(), off.get(), ids.get(), pts.get(),
                                        nullptr, nullptr, nbr.get());
   } else if (per_node <= 32) {

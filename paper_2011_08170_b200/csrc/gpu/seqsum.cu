@@ -180,37 +180,47 @@ __global__ void __launch_bounds__(256) k_ss_desc(SegGeom g, int64_t nchunks, con
   }
 }
 
+// one warp per super-chunk, one lane per chunk (kSuper == 32): combine the non-empty chunks'
+// descriptors in order (exclusive scan of Q shifts each chunk's min / max)
 __global__ void __launch_bounds__(256) k_ss_super(int64_t nsup_total, int64_t cps, int64_t sps,
                                                   const SumDesc* __restrict__ desc, SumDesc* __restrict__ sdesc) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  static_assert(kSuper == 32, "one lane per chunk");
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= nsup_total) return;
   const int64_t s = t / sps, j = t - s * sps;
-  const int64_t c0 = s * cps + j * kSuper, c1 = min64(c0 + kSuper, (s + 1) * cps);
+  const int64_t c = s * cps + j * kSuper + lane;
+  const bool have = c < (s + 1) * cps;
+  SumDesc d;
+  if (have) d = desc[c];
+  else d = SumDesc{0, 0, 0, 0, kEmpty};
+  const bool empty = (d.flags & kEmpty) != 0;
+  const unsigned ne = __ballot_sync(0xffffffffu, !empty);
   SumDesc r{0, 0, 0, -1, kEmpty};
-  bool bad = false;
-  for (int64_t c = c0; c < c1 && !bad; ++c) {
-    const SumDesc d = desc[c];
-    if (d.flags & kEmpty) continue;
-    if (d.flags & kBad) {
-      bad = true;
-      break;
+  if (ne) {
+    const int first = __ffs(ne) - 1;
+    const int be0 = __shfl_sync(0xffffffffu, d.be, first);
+    const int neg0 = __shfl_sync(0xffffffffu, d.flags & kNeg, first);
+    const bool ok = empty || (!(d.flags & kBad) && d.be == be0 && (d.flags & kNeg) == neg0);
+    const long long q = empty ? 0 : d.q;
+    long long incl = q;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    if (r.flags & kEmpty) {
-      r.be = d.be;
-      r.flags = d.flags & kNeg;
-      r.mn = d.mn;
-      r.mx = d.mx;
-      r.q = d.q;
-    } else if (d.be != r.be || (d.flags & kNeg) != (r.flags & kNeg)) {
-      bad = true;
-    } else {
-      r.mn = min(r.mn, r.q + d.mn);
-      r.mx = max(r.mx, r.q + d.mx);
-      r.q += d.q;
+    const long long excl = incl - q;
+    long long mn = empty ? LLONG_MAX : excl + d.mn, mx = empty ? LLONG_MIN : excl + d.mx;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
+    const long long total = __shfl_sync(0xffffffffu, incl, 31);
+    if (__all_sync(0xffffffffu, ok)) r = SumDesc{total, mn, mx, be0, neg0};
+    else r.flags = kBad;
   }
-  if (bad) r.flags = kBad;
-  sdesc[t] = r;
+  if (lane == 0) sdesc[t] = r;
 }
 
 // Warp 0 advances the exact running value over descriptors D[i..cnt), 32 at a time: a
@@ -347,7 +357,7 @@ void seq_sums_device(const double* v, int64_t k, int64_t seg_len, double* out, c
   launched("ss_scan");
   k_ss_desc<<<grid_for(nchunks * 32, 256), 256, 0, s>>>(g, nchunks, v, pre.get(), desc.get());
   launched("ss_desc");
-  k_ss_super<<<grid_for(nsup, 256), 256, 0, s>>>(nsup, g.cps, g.sps, desc.get(), sdesc.get());
+  k_ss_super<<<grid_for(nsup * 32, 256), 256, 0, s>>>(nsup, g.cps, g.sps, desc.get(), sdesc.get());
   launched("ss_super");
   k_ss_walk<<<(unsigned)nseg, kWalkThreads, 0, s>>>(g, v, desc.get(), sdesc.get(), out);
   launched("ss_walk");
