@@ -44,23 +44,23 @@ __global__ void __launch_bounds__(kShardThreads) k_shard_sweep(
       double s[B + 1];
 #pragma unroll
       for (int k = 0; k <= B; ++k) s[k] = CUDART_INF;
-      int j = 0;
-      for (; j + 4 <= w; j += 4) {  // 4 independent gathers in flight
-        int q[4];
-        double c[4], l[4];
+      // batches of 8 slots: 16 streaming loads (evict-first, so the L2 keeps the gathered
+      // multipliers) and then 8 independent gathers in flight per thread
+      for (int j = 0; j < w; j += 8) {
+        int q[8];
+        double c[8], l[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          q[u] = scol[base + (int64_t)(j + u) * 32];
-          c[u] = scost[base + (int64_t)(j + u) * 32];
+        for (int u = 0; u < 8; ++u) {
+          const bool ok = j + u < w;
+          const int64_t idx = base + (int64_t)(ok ? j + u : 0) * 32;
+          q[u] = ok ? __ldcs(scol + idx) : p;
+          c[u] = ok ? __ldcs(scost + idx) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) l[u] = lam[q[u]];
+        for (int u = 0; u < 8; ++u) l[u] = lam[q[u]];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) topk_bubble<B>(s, dsub(dsub(c[u], lv), l[u]));
-      }
-      for (; j < w; ++j) {
-        const int q = scol[base + (int64_t)j * 32];
-        topk_bubble<B>(s, dsub(dsub(scost[base + (int64_t)j * 32], lv), lam[q]));
+        for (int u = 0; u < 8; ++u)
+          if (j + u < w) topk_bubble<B>(s, dsub(dsub(c[u], lv), l[u]));
       }
       // delta_for (dual.cpp:63-68), lambda += eta * delta (dual.cpp:157-161)
       const double d = update ? dmul(0.5, dsub(s[B - 1], s[B])) : dmul(0.5, dadd(s[B - 1], s[B]));
