@@ -67,6 +67,18 @@ std::shared_ptr<Topology> make_topology(int n, int dev) {
 
 // ---------------------------------------------------------------- kernels
 
+int64_t* pinned_scratch() {
+  thread_local int64_t* p = nullptr;
+  if (!p) F2M_CUDA(cudaMallocHost(&p, 64 * sizeof(int64_t)));
+  return p;
+}
+
+__global__ void k_drop_sentinel(const int64_t* __restrict__ nsel, const uint64_t* __restrict__ keys,
+                                uint64_t sentinel, int64_t* __restrict__ out) {
+  const int64_t h = *nsel;
+  *out = (h > 0 && keys[h - 1] == sentinel) ? h - 1 : h;  // drop the "not halo" sentinel
+}
+
 __global__ void k_edge_keys(int64_t m, const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                             uint64_t* __restrict__ keys, int64_t* __restrict__ idx) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -279,13 +291,16 @@ __global__ void k_boundary(int64_t m, const int32_t* __restrict__ eu, const int3
 }
 
 __global__ void k_local_keys(int n, const int32_t* __restrict__ deg, const uint8_t* __restrict__ bnd,
-                             const int32_t* __restrict__ cos, uint64_t* __restrict__ key,
-                             int32_t* __restrict__ val, int32_t* __restrict__ nint) {
+                             const int32_t* __restrict__ cos, int dbits, int max_deg,
+                             uint64_t* __restrict__ key, int32_t* __restrict__ val, int32_t* __restrict__ nint) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int c = cos[p >> 5];
-  // CTA (keeps the partition), interior before boundary, then degree descending
-  key[p] = ((uint64_t)(uint32_t)c << 40) | ((uint64_t)bnd[p] << 32) | (uint32_t)(0x7fffffff - deg[p]);
+  // CTA (keeps the partition), interior before boundary, then degree descending (capped at
+  // max_deg: the local order only shapes the SELL padding, results do not depend on it), packed
+  // into bits(G) + 1 + dbits bits so the (stable) radix sort runs only the passes it needs
+  key[p] = ((uint64_t)(uint32_t)c << (dbits + 1)) | ((uint64_t)bnd[p] << dbits) |
+           (uint32_t)(max_deg - min(deg[p], max_deg));
   val[p] = p;
   if (!bnd[p]) atomicAdd(&nint[c], 1);
 }
@@ -311,8 +326,10 @@ __device__ __forceinline__ void own_range(int c, int n, const int32_t* __restric
 // one warp per slice: halo key (cta << 32 | q) for every neighbour q outside the owner's range
 __global__ void k_halo_keys(int n, int64_t nslices, const int64_t* __restrict__ sptr,
                             const int32_t* __restrict__ scol, const int32_t* __restrict__ seid,
-                            const int32_t* __restrict__ cos, const int32_t* __restrict__ lo,
-                            uint64_t* __restrict__ keys) {
+                            const int32_t* __restrict__ cos, const int32_t* __restrict__ lo, int qbits,
+                            uint64_t sentinel, uint64_t* __restrict__ keys) {
+  // key = (CTA << qbits) | position, packed so the radix sort runs only the passes it needs;
+  // non-halo slots get the sentinel (all ones: larger than every real key), sorted last
   const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;
@@ -322,16 +339,16 @@ __global__ void k_halo_keys(int n, int64_t nslices, const int64_t* __restrict__ 
   for (int64_t t = sptr[s] + lane; t < sptr[s + 1]; t += 32) {
     const int q = scol[t];
     const bool halo = seid[t] >= 0 && (q < p0 || q >= p1);
-    keys[t] = halo ? (((uint64_t)(uint32_t)c << 32) | (uint32_t)q) : ~0ULL;
+    keys[t] = halo ? (((uint64_t)(uint32_t)c << qbits) | (uint32_t)q) : sentinel;
   }
 }
 
-__global__ void k_halo_split(int64_t h, const uint64_t* __restrict__ keys, int32_t* __restrict__ halo,
+__global__ void k_halo_split(int64_t h, const uint64_t* __restrict__ keys, int qbits, int32_t* __restrict__ halo,
                              int32_t* __restrict__ cnt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= h) return;
-  halo[i] = (int32_t)(keys[i] & 0xffffffffu);
-  atomicAdd(&cnt[keys[i] >> 32], 1);
+  halo[i] = (int32_t)(keys[i] & ((1ull << qbits) - 1));
+  atomicAdd(&cnt[keys[i] >> qbits], 1);
 }
 
 __global__ void k_local_sizes(int ctas, int n, const int32_t* __restrict__ lo, const int32_t* __restrict__ hoff,
@@ -488,30 +505,34 @@ static void build_local_index(Topology& t) {
   launched("cta_of_slice");
   const int64_t slots = t.sell_slots;
   // halo entries
+  const int qbits = std::max(bit_width(n - 1), 1);
+  const int key_bits = bit_width(G) + qbits;  // 2^bit_width(G) > G - 1: the all-ones sentinel is unused
+  const uint64_t sentinel = (key_bits >= 64) ? ~0ULL : ((1ull << key_bits) - 1);
   DBuf<uint64_t> k0(std::max<int64_t>(slots, 1), s), k1(std::max<int64_t>(slots, 1), s);
   DBuf<int64_t> nsel(1, s);
   int64_t h = 0;
   if (slots > 0) {
     k_halo_keys<<<grid_for(t.nslices * 32, 256), 256, 0, s>>>(n, t.nslices, t.sptr.get(), t.scol.get(),
-                                                             t.seid.get(), cos.get(), t.cta_lo.get(), k0.get());
+                                                             t.seid.get(), cos.get(), t.cta_lo.get(), qbits,
+                                                             sentinel, k0.get());
     launched("halo_keys");
     size_t tmp = 0;
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), slots, 0, 64, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), slots, 0, key_bits, s));
     DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), slots, 0, 64, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), slots, 0, key_bits, s));
     launched("sort_halo");
     tmp = 0;
     F2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, k1.get(), k0.get(), nsel.get(), slots, s));
     DBuf<char> tb2(tmp, s);
     F2M_CUDA(cub::DeviceSelect::Unique(tb2.get(), tmp, k1.get(), k0.get(), nsel.get(), slots, s));
     launched("unique_halo");
-    F2M_CUDA(cudaMemcpyAsync(&h, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DBuf<int64_t> hcnt(1, s);
+    k_drop_sentinel<<<1, 1, 0, s>>>(nsel.get(), k0.get(), sentinel, hcnt.get());
+    launched("drop_sentinel");
+    int64_t* hs = pinned_scratch();
+    F2M_CUDA(cudaMemcpyAsync(hs, hcnt.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
-    uint64_t last = 0;
-    if (h > 0) {
-      F2M_CUDA(cudaMemcpy(&last, k0.get() + h - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost));
-      if (last == ~0ULL) --h;  // drop the "not halo" sentinel
-    }
+    h = hs[0];
   }
   t.halo.alloc(std::max<int64_t>(h, 1), s);
   t.halo_off.alloc(G + 1, s);
@@ -519,7 +540,7 @@ static void build_local_index(Topology& t) {
     DBuf<int32_t> cnt(G + 1, s);
     F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (G + 1), s));
     if (h > 0) {
-      k_halo_split<<<grid_for(h, 256), 256, 0, s>>>(h, k0.get(), t.halo.get(), cnt.get());
+      k_halo_split<<<grid_for(h, 256), 256, 0, s>>>(h, k0.get(), qbits, t.halo.get(), cnt.get());
       launched("halo_split");
     }
     size_t tmp = 0;
@@ -564,9 +585,9 @@ static void build_local_index(Topology& t) {
                                                              t.sdest.get(), t.row_nhalo.get());
     launched("halo_last");
   }
-  // CTA adjacency
+  // CTA adjacency (only the sweep-trace tooling reads it)
   t.nbr_off.alloc(G + 1, s);
-  {
+  if (std::getenv("F2M_SWEEP_TRACE")) {
     DBuf<uint64_t> nk(std::max<int64_t>(h, 1), s), nk2(std::max<int64_t>(h, 1), s);
     int64_t k = 0;
     if (h > 0) {
@@ -577,8 +598,10 @@ static void build_local_index(Topology& t) {
       DBuf<char> tb(tmp, s);
       F2M_CUDA(cub::DeviceSelect::Unique(tb.get(), tmp, nk.get(), nk2.get(), nsel.get(), h, s));
       launched("unique_nbr");
-      F2M_CUDA(cudaMemcpyAsync(&k, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      int64_t* hs = pinned_scratch();
+      F2M_CUDA(cudaMemcpyAsync(hs, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       F2M_CUDA(cudaStreamSynchronize(s));
+      k = hs[0];
     }
     t.nbr.alloc(std::max<int64_t>(k, 1), s);
     DBuf<int32_t> cnt(G + 1, s);
@@ -610,17 +633,20 @@ static void build_local_index(Topology& t) {
                                                   t.boff.get(), t.halo_pub.get());
       launched("halo_pub");
     }
-    F2M_CUDA(cudaMemcpyAsync(&t.nboundary, t.boff.get() + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaStreamSynchronize(s));
   }
   // [lam regions][halo ids (<= max_local ints)][resident: cost + local index per slot]
   const size_t lam_aligned = (lam_bytes + 15) & ~size_t(15);
   const size_t ids_bytes = (size_t)(lam_aligned / sizeof(double)) * sizeof(int);
-  // per-CTA slice table (v5): (slot offset, width) per slice, 16-byte aligned
+  // boundary count and the per-CTA slice table size (v5: (slot offset, width) per slice, 16-byte
+  // aligned) from one stream synchronisation
   int max_slices = 0;
   {
+    int32_t* hs = reinterpret_cast<int32_t*>(pinned_scratch());
+    F2M_CUDA(cudaMemcpyAsync(hs, t.boff.get() + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     std::vector<int32_t> lo(G + 1);
-    F2M_CUDA(cudaMemcpy(lo.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
+    F2M_CUDA(cudaMemcpyAsync(lo.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    t.nboundary = hs[0];
     for (int c = 0; c < G; ++c) max_slices = std::max(max_slices, lo[c + 1] - lo[c]);
   }
   const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int2) + (size_t)max_slices * 32;  // + row halo counts
@@ -683,13 +709,16 @@ void finalize_topology(Topology& t) {
     DBuf<uint64_t> k0(n, s), k1(n, s);
     DBuf<int32_t> v0(n, s), v1(n, s), deg2(n, s), ip2(n, s), p2(n, s), nint(G, s);
     F2M_CUDA(cudaMemsetAsync(nint.get(), 0, sizeof(int32_t) * G, s));
-    k_local_keys<<<grid_for(n, 256), 256, 0, s>>>(n, t.deg.get(), bnd.get(), cos.get(), k0.get(), v0.get(),
-                                                 nint.get());
+    constexpr int dbits = 7;  // degrees ordered exactly up to 127
+    const int key_bits = bit_width(std::max(G - 1, 1)) + 1 + dbits;
+    k_local_keys<<<grid_for(n, 256), 256, 0, s>>>(n, t.deg.get(), bnd.get(), cos.get(), dbits, (1 << dbits) - 1,
+                                                 k0.get(), v0.get(), nint.get());
     launched("local_keys");
     tmp = 0;
-    F2M_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.get(), k1.get(), v0.get(), v1.get(), n, 0, 64, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.get(), k1.get(), v0.get(), v1.get(), n, 0, key_bits, s));
     DBuf<char> tb2(tmp, s);
-    F2M_CUDA(cub::DeviceRadixSort::SortPairs(tb2.get(), tmp, k0.get(), k1.get(), v0.get(), v1.get(), n, 0, 64, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortPairs(tb2.get(), tmp, k0.get(), k1.get(), v0.get(), v1.get(), n, 0, key_bits,
+                                             s));
     launched("sort_local");
     k_window_apply<<<grid_for(n, 256), 256, 0, s>>>(n, v1.get(), t.deg.get(), t.iperm.get(), deg2.get(), ip2.get(),
                                                    p2.get());
@@ -705,23 +734,19 @@ void finalize_topology(Topology& t) {
     F2M_CUDA(cudaMemcpyAsync(t.cta_lo.get(), zero, sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s));
     F2M_CUDA(cudaMemcpyAsync(t.cta_int_hi.get(), zero, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   }
-  // min / max degree
+  // min / max degree and the SELL-32 layout; their sizes come back with ONE synchronisation
+  DBuf<int> mm(2, s);
   {
-    DBuf<int> mm(2, s);
-    int init[2] = {n > 0 ? INT_MAX : 0, 0};
-    F2M_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+    int* init = reinterpret_cast<int*>(pinned_scratch());
+    init[0] = n > 0 ? INT_MAX : 0;
+    init[1] = 0;
+    F2M_CUDA(cudaMemcpyAsync(mm.get(), init, 2 * sizeof(int), cudaMemcpyHostToDevice, s));
     if (n > 0) {
       k_minmax_deg<<<std::min<unsigned>(grid_for(n, 256), 1184), 256, 0, s>>>(n, t.deg.get(),
                                                                                mm.get(), mm.get() + 1);
       launched("minmax_deg");
     }
-    int out[2];
-    F2M_CUDA(cudaMemcpyAsync(out, mm.get(), sizeof(out), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaStreamSynchronize(s));
-    t.min_deg = out[0];
-    t.max_deg = out[1];
   }
-  // SELL-32 layout
   t.swidth.alloc(t.nslices, s);
   t.sptr.alloc(t.nslices + 1, s);
   DBuf<int64_t> ssize(t.nslices + 1, s);
@@ -740,8 +765,16 @@ void finalize_topology(Topology& t) {
   // exclusive scan over nslices+1 entries: sptr[nslices] = total padded slots (the last
   // input entry never contributes to an exclusive sum)
   int64_t slots = 0;
-  F2M_CUDA(cudaMemcpyAsync(&slots, t.sptr.get() + t.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
+  {
+    int64_t* hs = pinned_scratch();
+    F2M_CUDA(cudaMemcpyAsync(hs + 8, mm.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 9, t.sptr.get() + t.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    const int* mmh = reinterpret_cast<const int*>(hs + 8);
+    t.min_deg = mmh[0];
+    t.max_deg = mmh[1];
+    slots = hs[9];
+  }
   t.sell_slots = slots;
   t.scol.alloc(slots, s);
   t.seid.alloc(slots, s);

@@ -1314,7 +1314,7 @@ static void launch_init(const f2m_graph& g, double* d_lam, unsigned long long* l
   launched("init_local_midpoint");
 }
 
-void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam_pos) {
+void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam_pos, int* h_err_async) {
   const Topology& t = *g.topo;
   cudaStream_t s = t.stream;
   if (t.n == 0) return;
@@ -1336,6 +1336,10 @@ void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, doub
     case 6: launch_init<6>(g, d_lam_pos, llp, counter, err); break;
     case 7: launch_init<7>(g, d_lam_pos, llp, counter, err); break;
     default: launch_init<8>(g, d_lam_pos, llp, counter, err); break;
+  }
+  if (h_err_async) {  // pinned: the caller reads it after its next synchronisation
+    F2M_CUDA(cudaMemcpyAsync(h_err_async, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    return;
   }
   int herr = 0;
   F2M_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1495,11 +1499,15 @@ void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const 
   cudaStream_t s = t.stream;
   const auto t0 = std::chrono::steady_clock::now();
   DBuf<double> l0(std::max(t.n, 1), s), l1(std::max(t.n, 1), s);
+  int* init_err = nullptr;
   if (d_init) {
     if (t.n > 0)
       F2M_CUDA(cudaMemcpyAsync(l0.get(), d_init, sizeof(double) * t.n, cudaMemcpyDeviceToDevice, s));
   } else {
-    initial_state_device(g, cfg, l0.get());
+    // the init's watchdog flag is collected with the sweep's own synchronisation
+    init_err = reinterpret_cast<int*>(pinned_scratch() + 20);
+    *init_err = 0;
+    initial_state_device(g, cfg, l0.get(), init_err);
   }
   // threshold = eps * mean_cost (dual.cpp:221); with the mean still unknown the v5 kernel
   // computes it during the solve
@@ -1530,7 +1538,8 @@ void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const 
       }
     }
   }
-  rep.dual_value = dual_objective_device(g, result->get(), cfg.b);
+  rep.dual_value = dual_objective_device(g, result->get(), cfg.b);  // synchronises the stream
+  if (init_err && *init_err) throw Error(F2M_E_TIMEOUT, "initial-state kernel: dependency wait watchdog fired");
   d_lam_out = std::move(*result);
   rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

@@ -191,6 +191,21 @@ constexpr int kMaxComponentEdges = 20;  // primal.cpp:17
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+// Small page-locked host scratch (per thread, allocated once): device->host reads of several
+// scalars are queued asynchronously into it and collected with ONE stream synchronisation
+// (a D2H copy into pageable memory is itself synchronous).
+int64_t* pinned_scratch();  // >= 64 int64 slots
+
+// number of bits needed to represent v >= 0 (0 -> 0)
+inline int bit_width(int64_t v) {
+  int b = 0;
+  while (v > 0) {
+    ++b;
+    v >>= 1;
+  }
+  return b;
+}
+
 inline unsigned grid_for(int64_t items, int block) {
   int64_t g = (items + block - 1) / block;
   if (g < 1) g = 1;
@@ -221,7 +236,8 @@ void download_lambda(const f2m_graph& g, const double* d_lam_pos, double* h_lamb
 
 // dual.cu
 double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b);
-void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam_pos);
+void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam_pos,
+                          int* h_err_async = nullptr);
 struct SweepResult {
   int sweeps = 0;
   int converged = 0;

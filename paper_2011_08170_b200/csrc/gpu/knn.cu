@@ -260,23 +260,23 @@ __global__ void __launch_bounds__(128) k_knn_query_reg(int n, int rounded, const
   for (int j = 0; j < K; ++j) nbr[(int64_t)node * K + j] = hi[j];
 }
 
-__global__ void k_pair_keys(int n, int per_node, const int32_t* __restrict__ nbr,
+__global__ void k_pair_keys(int n, int per_node, int bits, const int32_t* __restrict__ nbr,
                             uint64_t* __restrict__ keys) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * per_node) return;
   const int i = (int)(t / per_node);
   const int q = nbr[t];
   const uint32_t a = (uint32_t)min(i, q), b = (uint32_t)max(i, q);
-  keys[t] = ((uint64_t)a << 32) | b;
+  keys[t] = ((uint64_t)a << bits) | b;  // (min, max) packed into 2*bits bits: short radix sort
 }
 
-__global__ void k_edges_from_keys(int64_t m, const uint64_t* __restrict__ keys,
+__global__ void k_edges_from_keys(int64_t m, const uint64_t* __restrict__ keys, int bits,
                                   const double* __restrict__ xy, int rounded,
                                   int32_t* __restrict__ eu, int32_t* __restrict__ ev,
                                   double* __restrict__ cost) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
-  const int u = (int)(keys[e] >> 32), v = (int)(keys[e] & 0xffffffffu);
+  const int u = (int)(keys[e] >> bits), v = (int)(keys[e] & ((1ull << bits) - 1));
   eu[e] = u;
   ev[e] = v;
   cost[e] = point_distance(xy[2 * u], xy[2 * u + 1], xy[2 * v], xy[2 * v + 1], rounded);
@@ -395,15 +395,15 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   // ---- symmetrize: sort + unique (graph.cpp:223-232)
   const int64_t np = (int64_t)n * per_node;
   DBuf<uint64_t> k0(np, s), k1(np, s);
-  k_pair_keys<<<grid_for(np, 256), 256, 0, s>>>(n, per_node, nbr.get(), k0.get());
+  int bits = 1;  // ids < 2^bits
+  while ((1LL << bits) < n) ++bits;
+  k_pair_keys<<<grid_for(np, 256), 256, 0, s>>>(n, per_node, bits, nbr.get(), k0.get());
   launched("pair_keys");
   {
     size_t tmp = 0;
-    int bits = 1;
-    while ((1LL << bits) < n) ++bits;
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), np, 0, 32 + bits, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), np, 0, 2 * bits, s));
     DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), np, 0, 32 + bits, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), np, 0, 2 * bits, s));
     launched("sort_pairs");
   }
   DBuf<int64_t> nsel(1, s);
@@ -421,7 +421,7 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   t.eu.alloc(m, s);
   t.ev.alloc(m, s);
   g->cost.alloc(m, s);
-  k_edges_from_keys<<<grid_for(m, 256), 256, 0, s>>>(m, k0.get(), d_xy, rounded, t.eu.get(), t.ev.get(),
+  k_edges_from_keys<<<grid_for(m, 256), 256, 0, s>>>(m, k0.get(), bits, d_xy, rounded, t.eu.get(), t.ev.get(),
                                                     g->cost.get());
   launched("edges_from_keys");
 
@@ -434,11 +434,12 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
     k_morton<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of.get(), gp.get(), mk0.get(), i0.get());
     launched("morton");
     size_t tmp = 0;
+    const int mbits = 2 * std::max(bit_width(std::max(hp.gx, hp.gy) - 1), 1);  // interleaved cell coordinates
     F2M_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, mk0.get(), mk1.get(), i0.get(), t.iperm.get(), n,
-                                             0, 64, s));
+                                             0, mbits, s));
     DBuf<char> tb(tmp, s);
     F2M_CUDA(cub::DeviceRadixSort::SortPairs(tb.get(), tmp, mk0.get(), mk1.get(), i0.get(), t.iperm.get(), n,
-                                             0, 64, s));
+                                             0, mbits, s));
     launched("sort_morton");
     k_invert<<<grid_for(n, 256), 256, 0, s>>>(n, t.iperm.get(), t.perm.get());
     launched("invert_perm");

@@ -86,17 +86,18 @@ __global__ void k_union(int64_t z, const int32_t* __restrict__ zedges, const int
 }
 
 __global__ void k_comp_keys(int64_t z, const int32_t* __restrict__ zedges, const int32_t* __restrict__ eu,
-                            int* parent, uint64_t* __restrict__ keys) {
+                            int* parent, int ebits, uint64_t* __restrict__ keys) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= z) return;
   const int e = zedges[i];
-  keys[i] = ((uint64_t)(uint32_t)uf_find(parent, eu[e]) << 32) | (uint32_t)e;
+  // (component root, edge id) packed into bits(n) + ebits bits: short radix sort
+  keys[i] = ((uint64_t)(uint32_t)uf_find(parent, eu[e]) << ebits) | (uint32_t)e;
 }
 
-__global__ void k_heads(int64_t z, const uint64_t* __restrict__ keys, uint8_t* __restrict__ head) {
+__global__ void k_heads(int64_t z, const uint64_t* __restrict__ keys, int ebits, uint8_t* __restrict__ head) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= z) return;
-  head[i] = (i == 0) || ((keys[i] >> 32) != (keys[i - 1] >> 32));
+  head[i] = (i == 0) || ((keys[i] >> ebits) != (keys[i - 1] >> ebits));
 }
 
 // solve_zero_component (primal.cpp:65-140) as an iterative DFS with the recursion's exact
@@ -104,12 +105,12 @@ __global__ void k_heads(int64_t z, const uint64_t* __restrict__ keys, uint8_t* _
 __device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __restrict__ eu,
                                 const int32_t* __restrict__ ev, const double* __restrict__ cost,
                                 const int32_t* __restrict__ residual, double* __restrict__ x,
-                                bool comp_is_sorted_keys, const uint64_t* keys) {
+                                bool comp_is_sorted_keys, const uint64_t* keys, int ebits) {
   int nodes[2 * kMaxComponentEdges];
   int nn = 0;
   int ce[kMaxComponentEdges];
   for (int i = 0; i < mc; ++i) {
-    ce[i] = comp_is_sorted_keys ? (int)(keys[i] & 0xffffffffu) : comp[i];
+    ce[i] = comp_is_sorted_keys ? (int)(keys[i] & ((1ull << ebits) - 1)) : comp[i];
     nodes[nn++] = eu[ce[i]];
     nodes[nn++] = ev[ce[i]];
   }
@@ -201,7 +202,7 @@ __device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __re
 __global__ void k_components(int64_t ncomp, int64_t z, const int32_t* __restrict__ heads,
                              const uint64_t* __restrict__ keys, const int32_t* __restrict__ eu,
                              const int32_t* __restrict__ ev, const double* __restrict__ cost,
-                             const int32_t* __restrict__ residual, double* __restrict__ x,
+                             const int32_t* __restrict__ residual, double* __restrict__ x, int ebits,
                              unsigned long long* __restrict__ fail) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= ncomp) return;
@@ -211,7 +212,7 @@ __global__ void k_components(int64_t ncomp, int64_t z, const int32_t* __restrict
     atomicMin(fail, ((unsigned long long)c << 32) | (unsigned long long)mc);
     return;
   }
-  if (!solve_component(nullptr, (int)mc, eu, ev, cost, residual, x, true, keys + lo)) {
+  if (!solve_component(nullptr, (int)mc, eu, ev, cost, residual, x, true, keys + lo, ebits)) {
     atomicMin(fail, ((unsigned long long)c << 32) | (unsigned long long)(0x80000000u | (unsigned)mc));
   }
 }
@@ -220,7 +221,7 @@ __global__ void k_one_component(int mc, const int32_t* __restrict__ comp, const 
                                 const int32_t* __restrict__ ev, const double* __restrict__ cost,
                                 const int32_t* __restrict__ residual, double* __restrict__ x,
                                 int* __restrict__ ok) {
-  *ok = solve_component(comp, mc, eu, ev, cost, residual, x, false, nullptr) ? 1 : 0;
+  *ok = solve_component(comp, mc, eu, ev, cost, residual, x, false, nullptr, 32) ? 1 : 0;
 }
 
 __global__ void k_products(int64_t m, const double* __restrict__ cost, const double* __restrict__ x,
@@ -313,17 +314,18 @@ void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, dou
   k_union<<<grid_for(z, 256), 256, 0, s>>>(z, zedges.get(), t.eu.get(), t.ev.get(), parent.get());
   launched("union_find");
   DBuf<uint64_t> k0(z, s), k1(z, s);
-  k_comp_keys<<<grid_for(z, 256), 256, 0, s>>>(z, zedges.get(), t.eu.get(), parent.get(), k0.get());
+  const int ebits = std::max(bit_width(m - 1), 1), key_bits = ebits + std::max(bit_width(n - 1), 1);
+  k_comp_keys<<<grid_for(z, 256), 256, 0, s>>>(z, zedges.get(), t.eu.get(), parent.get(), ebits, k0.get());
   launched("comp_keys");
   {
     size_t tmp = 0;
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), z, 0, 64, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), z, 0, key_bits, s));
     DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), z, 0, 64, s));
+    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), z, 0, key_bits, s));
     launched("sort_components");
   }
   DBuf<uint8_t> head(z, s);
-  k_heads<<<grid_for(z, 256), 256, 0, s>>>(z, k1.get(), head.get());
+  k_heads<<<grid_for(z, 256), 256, 0, s>>>(z, k1.get(), ebits, head.get());
   launched("heads");
   DBuf<int32_t> zi(z, s), heads(z, s);
   k_iota_n<<<grid_for(z, 256), 256, 0, s>>>((int)z, zi.get());
@@ -332,7 +334,7 @@ void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, dou
   DBuf<unsigned long long> fail(1, s);
   F2M_CUDA(cudaMemsetAsync(fail.get(), 0xff, sizeof(unsigned long long), s));
   k_components<<<grid_for(ncomp, 64), 64, 0, s>>>(ncomp, z, heads.get(), k1.get(), t.eu.get(), t.ev.get(),
-                                                  g.cost.get(), residual.get(), d_x, fail.get());
+                                                  g.cost.get(), residual.get(), d_x, ebits, fail.get());
   launched("zero_components");
   unsigned long long hf = 0;
   F2M_CUDA(cudaMemcpyAsync(&hf, fail.get(), sizeof(hf), cudaMemcpyDeviceToHost, s));
