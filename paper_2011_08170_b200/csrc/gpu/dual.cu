@@ -24,6 +24,8 @@
 #include <cstdlib>
 #include <string>
 
+#include <cstring>
+
 #include "internal.cuh"
 
 namespace f2mgpu {
@@ -1192,11 +1194,16 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       launched("gdp_sweep5");
     }
     F2M_CUDA(cudaEventRecord(e1, s));
-    Sweep4Ctl h;
-    F2M_CUDA(cudaMemcpyAsync(&h, ctl.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
-    double hmean = 0.0;
-    if (defer_eps > 0.0) F2M_CUDA(cudaMemcpyAsync(&hmean, mean_out.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    // control block and deferred mean through page-locked scratch: one synchronisation
+    static_assert(sizeof(Sweep4Ctl) <= 16 * sizeof(int64_t), "pinned scratch layout");
+    int64_t* ps = pinned_scratch();
+    F2M_CUDA(cudaMemcpyAsync(ps + 32, ctl.get(), sizeof(Sweep4Ctl), cudaMemcpyDeviceToHost, s));
+    if (defer_eps > 0.0) F2M_CUDA(cudaMemcpyAsync(ps + 48, mean_out.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
+    Sweep4Ctl h;
+    std::memcpy(&h, ps + 32, sizeof(h));
+    double hmean = 0.0;
+    if (defer_eps > 0.0) std::memcpy(&hmean, ps + 48, sizeof(double));
     if (defer_eps > 0.0 && !h.abort) {
       g.mean_cost = hmean;  // bit-identical to sequential_mean (same chain, same order)
       g.mean_known = true;
@@ -1210,8 +1217,8 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       F2M_CUDA(cudaMemcpyAsync(d_lam1, a.gl + (size_t)outbuf * a.gstride, sizeof(double) * t.n,
                                cudaMemcpyDeviceToDevice, s));
     outbuf = 1;
-    F2M_CUDA(cudaStreamSynchronize(s));
     if (a.trace) {
+      F2M_CUDA(cudaStreamSynchronize(s));
       std::vector<unsigned long long> hbuf(trace.n);
       F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
       if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
@@ -1425,7 +1432,7 @@ __global__ void k_dual_combine(int nchunks_node, int nchunks_edge, int b, const 
   *out = dadd(dmul((double)b, ns), es);
 }
 
-double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b) {
+double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b, double* h_async) {
   const Topology& t = *g.topo;
   cudaStream_t s = t.stream;
   const int nn = (int)((t.n + kNodeChunk - 1) / kNodeChunk);
@@ -1442,6 +1449,10 @@ double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b)
   }
   k_dual_combine<<<1, 1, 0, s>>>(nn, ne, b, parts.get(), parts.get() + nn + ne);
   launched("dual_combine");
+  if (h_async) {
+    F2M_CUDA(cudaMemcpyAsync(h_async, parts.get() + nn + ne, sizeof(double), cudaMemcpyDeviceToHost, s));
+    return NAN;
+  }
   double h = 0.0;
   F2M_CUDA(cudaMemcpyAsync(&h, parts.get() + nn + ne, sizeof(double), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
@@ -1493,7 +1504,7 @@ static double gs_sweep_device(const f2m_graph& g, const f2m_engine_config& cfg, 
 }
 
 void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const double* d_init,
-                        DBuf<double>& d_lam_out, f2m_convergence_report& rep) {
+                        DBuf<double>& d_lam_out, f2m_convergence_report& rep, double* h_dual_async) {
   validate_engine(cfg);
   const Topology& t = *g.topo;
   cudaStream_t s = t.stream;
@@ -1538,8 +1549,11 @@ void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const 
       }
     }
   }
-  rep.dual_value = dual_objective_device(g, result->get(), cfg.b);  // synchronises the stream
-  if (init_err && *init_err) throw Error(F2M_E_TIMEOUT, "initial-state kernel: dependency wait watchdog fired");
+  rep.dual_value = dual_objective_device(g, result->get(), cfg.b, h_dual_async);
+  if (init_err) {  // collected by the sweep's (or, without sweeps, this) synchronisation
+    if (cfg.max_sweeps <= 0 || cfg.mode != 0) F2M_CUDA(cudaStreamSynchronize(s));
+    if (*init_err) throw Error(F2M_E_TIMEOUT, "initial-state kernel: dependency wait watchdog fired");
+  }
   d_lam_out = std::move(*result);
   rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

@@ -193,8 +193,10 @@ __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return
 
 // Small page-locked host scratch (per thread, allocated once): device->host reads of several
 // scalars are queued asynchronously into it and collected with ONE stream synchronisation
-// (a D2H copy into pageable memory is itself synchronous).
-int64_t* pinned_scratch();  // >= 64 int64 slots
+// (a D2H copy into pageable memory is itself synchronous). 64 int64 slots: 0-15 topology
+// build, 20 init watchdog, 24 dual objective, 26-28 certification, 32-47 sweep control
+// block, 48 deferred mean.
+int64_t* pinned_scratch();
 
 // number of bits needed to represent v >= 0 (0 -> 0)
 inline int bit_width(int64_t v) {
@@ -235,7 +237,9 @@ void upload_lambda(const f2m_graph& g, const double* h_lambda, double* d_lam_pos
 void download_lambda(const f2m_graph& g, const double* d_lam_pos, double* h_lambda);
 
 // dual.cu
-double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b);
+// h_async (page-locked) != nullptr: the value is copied there asynchronously (valid after the
+// stream's next synchronisation) and NaN is returned
+double dual_objective_device(const f2m_graph& g, const double* d_lam_pos, int b, double* h_async = nullptr);
 void initial_state_device(const f2m_graph& g, const f2m_engine_config& cfg, double* d_lam_pos,
                           int* h_err_async = nullptr);
 struct SweepResult {
@@ -250,8 +254,9 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
                        double* d_lam1, int max_sweeps, double threshold, double* d_record,
                        double defer_eps = 0.0);
 void validate_engine(const f2m_engine_config& cfg);
+// h_dual_async: see dual_objective_device (rep.dual_value is then left NaN for the caller)
 void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const double* d_init,
-                        DBuf<double>& d_lam_out, f2m_convergence_report& rep);
+                        DBuf<double>& d_lam_out, f2m_convergence_report& rep, double* h_dual_async = nullptr);
 
 // primal.cu
 void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, double* d_x);
@@ -259,6 +264,9 @@ double objective_device(const f2m_graph& g, const double* d_x);
 void verify_device(const f2m_graph& g, const double* d_x, double objective,
                    const double* d_lam_pos, f2m_verification& rep, int32_t* h_nodes,
                    double* h_sums, int32_t* h_vals, int64_t capacity, const double* dual_known = nullptr);
+// objective + feasibility counts of the certified pipeline (no violation lists) with ONE
+// synchronisation; dual: the dual objective (already known) for the gap
+void certify_device(const f2m_graph& g, const double* d_x, double dual, double& objective, f2m_verification& rep);
 
 // persistent sweep launch geometry (dual.cu)
 int sweep_grid_ctas(int dev);

@@ -14,6 +14,8 @@
 //                by the parallel exact-sequential-sum primitive (seqsum.cu).
 //  verify        per-node sums over the SELL rows (all partial sums are exact multiples of
 //                1/2), value-set check, gap = objective - g(lambda) (primal.cpp:235-276).
+#include <cstring>
+
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -252,6 +254,31 @@ __global__ void k_value_check(int64_t m, const double* __restrict__ x, uint8_t* 
   bad[e] = v != 0.0 && v != 0.5 && v != 1.0;
 }
 
+// certification counts (no lists): per-node sum != 2.0 (primal.cpp:249-258) and values outside
+// {0, 1/2, 1} (primal.cpp:259-266), warp-aggregated atomics
+__global__ void k_certify_counts(int n, int64_t m, const int32_t* __restrict__ perm, const int32_t* __restrict__ deg,
+                                 const int64_t* __restrict__ sptr, const int32_t* __restrict__ seid,
+                                 const double* __restrict__ x, unsigned long long* __restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool nb = false, vb = false;
+  if (i < n) {
+    const int p = perm[i];
+    const int64_t base = sptr[p >> 5] + (p & 31);
+    double sum = 0.0;
+    for (int j = 0; j < deg[p]; ++j) sum = dadd(sum, x[seid[base + (int64_t)j * 32]]);
+    nb = sum != 2.0;
+  }
+  if (i < m) {
+    const double v = x[i];
+    vb = v != 0.0 && v != 0.5 && v != 1.0;
+  }
+  const unsigned bn = __ballot_sync(0xffffffffu, nb), bv = __ballot_sync(0xffffffffu, vb);
+  if ((threadIdx.x & 31) == 0) {
+    if (bn) atomicAdd(counts, (unsigned long long)__popc(bn));
+    if (bv) atomicAdd(counts + 1, (unsigned long long)__popc(bv));
+  }
+}
+
 template <class T>
 static int64_t select_flagged(const T* in, const uint8_t* flags, T* out, int64_t count, cudaStream_t s) {
   DBuf<int64_t> nsel(1, s);
@@ -408,6 +435,38 @@ void verify_device(const f2m_graph& g, const double* d_x, double objective, cons
   // dual_objective(graph, state) (primal.cpp:274); solve_duals already computed it for the same
   // graph, lambda and b when the caller passes it in
   rep.duality_gap = objective - (dual_known ? *dual_known : dual_objective_device(g, d_lam_pos, 2));
+}
+
+void certify_device(const f2m_graph& g, const double* d_x, double dual, double& objective, f2m_verification& rep) {
+  const Topology& t = *g.topo;
+  cudaStream_t s = t.stream;
+  const int n = t.n;
+  const int64_t m = t.m;
+  DBuf<unsigned long long> counts(2, s);
+  DBuf<double> obj(1, s);
+  F2M_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(unsigned long long), s));
+  F2M_CUDA(cudaMemsetAsync(obj.get(), 0, sizeof(double), s));
+  if (m > 0) {
+    DBuf<double> prod(m, s);
+    k_products<<<grid_for(m, 256), 256, 0, s>>>(m, g.cost.get(), d_x, prod.get());
+    launched("products");
+    seq_sums_device(prod.get(), m, m, obj.get(), s);  // the reference's left-to-right chain, exactly
+  }
+  const int64_t items = std::max<int64_t>(n, m);
+  if (items > 0) {
+    k_certify_counts<<<grid_for(items, 256), 256, 0, s>>>(n, m, t.perm.get(), t.deg.get(), t.sptr.get(),
+                                                         t.seid.get(), d_x, counts.get());
+    launched("certify_counts");
+  }
+  int64_t* ps = pinned_scratch();
+  F2M_CUDA(cudaMemcpyAsync(ps + 26, obj.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  F2M_CUDA(cudaMemcpyAsync(ps + 27, counts.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  F2M_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(&objective, ps + 26, sizeof(double));
+  rep.violated_count = ps[27];
+  rep.value_violation_count = ps[28];
+  rep.feasible = ps[27] == 0 && ps[28] == 0;
+  rep.duality_gap = objective - dual;  // primal.cpp:274
 }
 
 }  // namespace f2mgpu

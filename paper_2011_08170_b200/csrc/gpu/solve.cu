@@ -8,6 +8,8 @@
 #include <chrono>
 #include <sstream>
 
+#include <cstring>
+
 #include "internal.cuh"
 
 namespace f2mgpu {
@@ -60,7 +62,11 @@ static void full_solve_graph_device(const f2m_graph& g, const f2m_run_config& rc
     auto ts = std::chrono::steady_clock::now();
     f2m_convergence_report conv{};
     DBuf<double> lam;
-    solve_duals_device(attempt, rc.engine, nullptr, lam, conv);
+    // restart 0 solves g itself with b = 2: its dual objective is the certificate's g(lambda);
+    // it is read back (page-locked, asynchronously) with the extraction's synchronisations
+    const bool same = jit == nullptr && rc.engine.b == 2;
+    double* dual_async = reinterpret_cast<double*>(pinned_scratch() + 24);
+    solve_duals_device(attempt, rc.engine, nullptr, lam, conv, dual_async);
     t_duals += seconds_since(ts);
 
     ts = std::chrono::steady_clock::now();
@@ -74,12 +80,12 @@ static void full_solve_graph_device(const f2m_graph& g, const f2m_run_config& rc
       continue;
     }
     // certify against the unperturbed costs (solve.cpp:74-83)
-    const double objective = objective_device(g, x.get());
+    const double dual = same ? 0.0 : dual_objective_device(g, lam.get(), 2);
+    double objective = 0.0;
     f2m_verification ver{};
-    // restart 0 solved on g itself with b = 2: its report already holds dual_objective(g, lambda)
-    const bool same = jit == nullptr && rc.engine.b == 2;
-    verify_device(g, x.get(), objective, lam.get(), ver, nullptr, nullptr, nullptr, 0,
-                  same ? &conv.dual_value : nullptr);
+    certify_device(g, x.get(), 0.0, objective, ver);  // synchronises: the async dual is valid now
+    std::memcpy(&conv.dual_value, dual_async, sizeof(double));
+    ver.duality_gap = objective - (same ? conv.dual_value : dual);
     t_extract += seconds_since(ts);
     const double scale = 1.0 + std::fabs(objective);
     if (ver.feasible && ver.duality_gap <= rc.gap_tol * scale) {
