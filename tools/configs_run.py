@@ -7,6 +7,7 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2011_08170_b200 as f2m  # noqa: E402
+import torch  # noqa: E402
 
 CONFIGS = [
     ("uniform 1k seed 1", "u", 1000, 1, 1e-9),
@@ -22,10 +23,14 @@ for name, kind, n, seed, eps in CONFIGS:
     if only and not any(o in name for o in only):
         continue
     gen = f2m.generate_clustered_instance if kind == "c" else f2m.generate_instance
-    xy = gen(n, seed).points_array()
-    f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=200000) if n <= 200000 else None  # warm-up
+    # page-locked input and result buffers (as bench.py's e2e leg)
+    xy = torch.from_numpy(gen(n, seed).points_array()).pin_memory().numpy()
+    xo = torch.empty(n * 10 + 1, dtype=torch.float64).pin_memory().numpy()
+    lo = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    if n <= 200000:  # warm-up
+        f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=200000, out_value=xo, out_duals=lo)
     t0 = time.perf_counter()
-    r = f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=400000)
+    r = f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=400000, out_value=xo, out_duals=lo)
     wall = time.perf_counter() - t0
     ms, sw = f2m.last_sweep_kernel()
     print(json.dumps({"config": name, "n": n, "m": int(r["graph"].m), "wall_s": wall, "t_total": r["t_total"],
