@@ -86,6 +86,16 @@ def test_random_shapes_vs_oracle(f2m, orc, n, k, rounded):
     _same_as_oracle(f2m, orc, xy, k, rounded)
 
 
+@pytest.mark.parametrize("k", list(range(3, 17)))
+def test_every_candidate_count_vs_oracle(f2m, orc, k):
+    """k = 3..12 run the register-resident k_knn_query_reg<K>, 13..16 the generic list; both
+    must give the reference's lists, including (distance, id) tie-breaks on an integer grid."""
+    xy = orc.generate_instance(1200, 77 + k, 500.0)
+    _same_as_oracle(f2m, orc, xy, k, k % 2 == 0)
+    xs, ys = np.meshgrid(np.arange(24.0), np.arange(17.0))
+    _same_as_oracle(f2m, orc, np.stack([xs.ravel(), ys.ravel()], 1), k, False)
+
+
 def test_clustered_generator_vs_oracle(f2m, orc):
     inst = f2m.generate_clustered_instance(20000, 5)
     xy = inst.points_array()
