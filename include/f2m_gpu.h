@@ -288,6 +288,40 @@ int f2m_ids_to_positions(const f2m_graph* g, const double* d_ids, double* d_pos,
  * (dual.cpp:96-109, parallel.cpp chunking) and mean_cost (graph.cpp:47-49). */
 int f2m_seq_sums(const double* d_v, int64_t k, int64_t seg_len, double* d_out, void* stream);
 
+/* ---- fused peer-memory node-sharded solve (SURVEY.md §8(e) "faster fused variant") ----------
+ * One persistent kernel per rank runs every sweep of jacobi_sweep / solve_duals (dual.cpp:129-167,
+ * :210-246) on the rank's rows; halo multipliers are stored straight into the reader's receive
+ * buffer (peer memory, LL words), sweep maxima into every rank's board; all ranks take the same
+ * stop decision. Buffers (recv: 2 x n_recv x 16 B, board: 4 x world x 16 B) must be zeroed on
+ * every rank before any rank launches. The plan lists follow HaloPlan (sharded.py): recv_pos =
+ * positions this rank reads, grouped by owner; send_* = (own position, reader rank, index in the
+ * reader's recv list). The launch is asynchronous (ranks must run concurrently). */
+typedef struct {
+  const int32_t* d_recv_pos;
+  int64_t n_recv;
+  unsigned long long* d_recv_buf;
+  const int32_t* d_send_pos;
+  const int32_t* d_send_peer;
+  const int32_t* d_send_dst;
+  int64_t n_send;
+  unsigned long long* const* d_peer_recv; /* [world] device pointers */
+  const int64_t* d_peer_nrecv;            /* [world] */
+  unsigned long long* d_board;
+  unsigned long long* const* d_peer_board; /* [world] device pointers */
+} f2m_p2p_plan;
+typedef struct {
+  int sweeps;
+  int converged;
+  int out_buffer; /* 0: lambda_{k+1} is in d_lam_a, 1: in d_lam_b (own positions) */
+  double final_max_abs_delta;
+} f2m_p2p_result;
+size_t f2m_p2p_ctl_bytes(void);
+/* co-resident CTAs of the p2p kernel on the current device (all SMs x occupancy); < 0: -status */
+int f2m_p2p_max_ctas(int b);
+int f2m_p2p_launch(const f2m_shard* s, const f2m_engine_config* cfg, const f2m_p2p_plan* plan, double* d_lam_a,
+                   double* d_lam_b, double threshold, int max_sweeps, int ctas, void* d_ctl, void* stream);
+int f2m_p2p_get_result(const void* d_ctl, f2m_p2p_result* out);
+
 /* ---- instrumentation (bench.py / tests) ----------------------------------------------- */
 /* Number of kernels this library launched since load (all entry points). */
 uint64_t f2m_kernel_launch_count(void);

@@ -442,7 +442,46 @@ PYBIND11_MODULE(_f2m, m) {
                                         reinterpret_cast<unsigned long long*>(max_bits),
                                         reinterpret_cast<void*>(stream)));
            },
-           py::arg("lam_full"), py::arg("lam_shard"), py::arg("max_bits"), py::arg("stream") = 0);
+           py::arg("lam_full"), py::arg("lam_shard"), py::arg("max_bits"), py::arg("stream") = 0)
+      // fused peer-memory solve (f2m_p2p_launch): all pointers are device addresses (integers)
+      .def("p2p_launch",
+           [](const Shard& sh, std::uintptr_t recv_pos, std::int64_t n_recv, std::uintptr_t recv_buf,
+              std::uintptr_t send_pos, std::uintptr_t send_peer, std::uintptr_t send_dst, std::int64_t n_send,
+              std::uintptr_t peer_recv, std::uintptr_t peer_nrecv, std::uintptr_t board, std::uintptr_t peer_board,
+              std::uintptr_t lam_a, std::uintptr_t lam_b, double threshold, int max_sweeps, int ctas,
+              std::uintptr_t ctl, std::uintptr_t stream) {
+             f2m_p2p_plan pl{};
+             pl.d_recv_pos = reinterpret_cast<const int32_t*>(recv_pos);
+             pl.n_recv = n_recv;
+             pl.d_recv_buf = reinterpret_cast<unsigned long long*>(recv_buf);
+             pl.d_send_pos = reinterpret_cast<const int32_t*>(send_pos);
+             pl.d_send_peer = reinterpret_cast<const int32_t*>(send_peer);
+             pl.d_send_dst = reinterpret_cast<const int32_t*>(send_dst);
+             pl.n_send = n_send;
+             pl.d_peer_recv = reinterpret_cast<unsigned long long* const*>(peer_recv);
+             pl.d_peer_nrecv = reinterpret_cast<const int64_t*>(peer_nrecv);
+             pl.d_board = reinterpret_cast<unsigned long long*>(board);
+             pl.d_peer_board = reinterpret_cast<unsigned long long* const*>(peer_board);
+             f2m::check(f2m_p2p_launch(sh.h, &sh.cfg, &pl, reinterpret_cast<double*>(lam_a),
+                                       reinterpret_cast<double*>(lam_b), threshold, max_sweeps, ctas,
+                                       reinterpret_cast<void*>(ctl), reinterpret_cast<void*>(stream)));
+           },
+           py::arg("recv_pos"), py::arg("n_recv"), py::arg("recv_buf"), py::arg("send_pos"), py::arg("send_peer"),
+           py::arg("send_dst"), py::arg("n_send"), py::arg("peer_recv"), py::arg("peer_nrecv"), py::arg("board"),
+           py::arg("peer_board"), py::arg("lam_a"), py::arg("lam_b"), py::arg("threshold"), py::arg("max_sweeps"),
+           py::arg("ctas"), py::arg("ctl"), py::arg("stream") = 0);
+  m.def("p2p_ctl_bytes", []() { return f2m_p2p_ctl_bytes(); });
+  m.def("p2p_max_ctas", [](int b) {
+    const int v = f2m_p2p_max_ctas(b);
+    if (v < 0) f2m::check(-v);
+    return v;
+  }, py::arg("b") = 2);
+  m.def("p2p_result", [](std::uintptr_t ctl) {
+    f2m_p2p_result r{};
+    f2m::check(f2m_p2p_get_result(reinterpret_cast<const void*>(ctl), &r));
+    return py::dict(py::arg("sweeps") = r.sweeps, py::arg("converged") = (bool)r.converged,
+                    py::arg("out_buffer") = r.out_buffer, py::arg("final_max_abs_delta") = r.final_max_abs_delta);
+  });
   m.def(
       "shard_create",
       [](const f2m::Graph& graph, int rank, int world, int b, double eta, const std::string& update) {

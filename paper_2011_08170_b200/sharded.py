@@ -311,11 +311,14 @@ def solve_duals_sharded(graph, comm=None, eps: float = 1e-9, max_sweeps: int = 2
 
     comm: TorchDistComm() inside an initialised NCCL process group (one GPU per rank), or
     LocalComm(world) to run `world` shards in this process on the current device.
-    exchange: "halo" (all-to-all of the values other ranks read, default) or "allgather" (the
-    whole vector every sweep). Returns (lambda in node-id order as numpy, report dict) on every
+    exchange: "halo" (all-to-all of the values other ranks read, default), "allgather" (the
+    whole vector every sweep) or "p2p" (one persistent kernel per rank for all sweeps, halo
+    multipliers and sweep maxima stored straight into the peers' memory; see _solve_duals_p2p). Returns (lambda in node-id order as numpy, report dict) on every
     rank."""
     if exchange == "halo":
         return _solve_duals_halo(graph, comm, eps, max_sweeps, b, eta, update, init, chunk, threshold)
+    if exchange == "p2p":
+        return _solve_duals_p2p(graph, comm, eps, max_sweeps, b, eta, update, init, threshold)
     from . import _f2m
 
     if comm is None:
@@ -415,3 +418,163 @@ def _solve_duals_halo(graph, comm, eps, max_sweeps, b, eta, update, init, chunk,
               "world": comm.world, "stride": stride, "exchange": "halo",
               "halo_values_per_sweep": meta["halo_values_per_sweep"]}
     return lam, report
+
+
+def p2p_plan_arrays(plans: Sequence[HaloPlan], rank: int):
+    """Flat send / receive lists of `rank` for the fused peer-memory solve: recv_pos (positions
+    this rank reads, grouped by owner), and per value it sends: own position, reader rank and the
+    index of that value in the reader's receive list (both sides sort by position)."""
+    world = len(plans)
+    recv_pos = plans[rank].recv_pos.astype(np.int32)
+    send_pos, send_peer, send_dst = [], [], []
+    off = 0
+    for r in range(world):
+        cnt = plans[rank].send_counts[r]
+        if cnt:
+            seg = plans[rank].send_pos[off:off + cnt]
+            base = int(sum(plans[r].recv_counts[:rank]))  # owner `rank`'s segment in r's receive list
+            assert plans[r].recv_counts[rank] == cnt
+            send_pos.append(seg)
+            send_peer.append(np.full(cnt, r, np.int32))
+            send_dst.append(base + np.arange(cnt, dtype=np.int32))
+        off += cnt
+    cat = (lambda xs: np.concatenate(xs).astype(np.int32)) if send_pos else (lambda xs: np.zeros(0, np.int32))
+    return recv_pos, cat(send_pos), cat(send_peer), cat(send_dst)
+
+
+class ShardedP2P:
+    """Fused peer-memory solve (SURVEY §8(e) "faster fused variant"): every rank launches ONE
+    persistent kernel (f2m_p2p_launch) that runs all sweeps of its rows; halo multipliers and
+    sweep maxima are stored straight into the other ranks' receive buffers / boards (NVLink peer
+    memory from torch symmetric memory across processes; plain device memory for LocalComm ranks,
+    which run concurrently on one GPU, each on its own stream). Bit-identical to one GPU.
+
+    Build once per graph; run(lam0_full, threshold, max_sweeps) -> (lam_full in position order,
+    result dict) may be called repeatedly (buffers are re-zeroed and ranks re-synchronised)."""
+
+    def __init__(self, graph, comm, b: int = 2, eta: float = 0.5, update: str = "midpoint", ctas: int = 0):
+        from . import _f2m
+
+        self._f2m = _f2m
+        self.comm = comm
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        dev = self.dev
+        self.world = world = comm.world
+        self.local = local = not isinstance(comm, TorchDistComm)
+        self.ranks = ranks = list(range(world)) if local else [comm.rank]
+        self.shards = {r: _f2m.shard_create(graph, r, world, b, eta, update) for r in ranks}
+        info = next(iter(self.shards.values())).info()
+        self.n, self.stride = n, stride = info["n"], info["stride"]
+        pos = graph.positions()
+        u, v, _ = graph.edge_arrays()
+        plans = halo_plans(n, world, stride, pos[u], pos[v])
+        nrecv = [len(p.recv_pos) for p in plans]
+        self.halo_values = int(sum(nrecv))
+        recv_words = 2 * 2 * max(max(nrecv), 1)  # 2 parities x LL pair (2 words) per value
+        board_words = 4 * world * 2
+        if local:
+            self.recv_bufs = {r: torch.zeros(recv_words, dtype=torch.int64, device=dev) for r in ranks}
+            self.boards = {r: torch.zeros(board_words, dtype=torch.int64, device=dev) for r in ranks}
+            recv_ptrs = [self.recv_bufs[r].data_ptr() for r in range(world)]
+            board_ptrs = [self.boards[r].data_ptr() for r in range(world)]
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            group = comm.group if comm.group is not None else dist.group.WORLD
+            rb = symm_mem.empty(recv_words, dtype=torch.int64, device=dev)
+            bd = symm_mem.empty(board_words, dtype=torch.int64, device=dev)
+            self._handles = (symm_mem.rendezvous(rb, group), symm_mem.rendezvous(bd, group))
+            self.recv_bufs, self.boards = {comm.rank: rb}, {comm.rank: bd}
+            recv_ptrs, board_ptrs = list(self._handles[0].buffer_ptrs), list(self._handles[1].buffer_ptrs)
+        self.peer_recv = torch.tensor(recv_ptrs, dtype=torch.int64, device=dev)
+        self.peer_board = torch.tensor(board_ptrs, dtype=torch.int64, device=dev)
+        self.peer_nrecv = torch.tensor(nrecv, dtype=torch.int64, device=dev)
+        # every local rank's grid co-resident: the device's CTA capacity split between them
+        self.ctas = ctas or max(1, _f2m.p2p_max_ctas(b) // len(ranks))
+        self.per = {}
+        for r in ranks:
+            rp, sp, speer, sdst = p2p_plan_arrays(plans, r)
+            t = lambda x: torch.from_numpy(np.ascontiguousarray(x if len(x) else np.zeros(1, np.int32))).to(dev)  # noqa: E731
+            self.per[r] = dict(rp=t(rp), nr=len(rp), sp=t(sp), speer=t(speer), sdst=t(sdst), ns=len(sp),
+                               a=torch.empty(stride * world, dtype=torch.float64, device=dev),
+                               b=torch.empty(stride * world, dtype=torch.float64, device=dev),
+                               ctl=torch.zeros(_f2m.p2p_ctl_bytes() // 8 + 1, dtype=torch.int64, device=dev),
+                               stream=torch.cuda.Stream(dev))
+
+    def launch(self, lam0_full: torch.Tensor, threshold: float, max_sweeps: int, ev_start=None, ev_end=None) -> None:
+        """Zero the exchange buffers, synchronise the ranks, launch every local rank's kernel
+        (optionally bracketed by CUDA events on the current stream)."""
+        for r in self.ranks:
+            self.recv_bufs[r].zero_()
+            self.boards[r].zero_()
+            self.per[r]["a"].copy_(lam0_full)
+        torch.cuda.synchronize(self.dev)  # buffers zeroed before any rank publishes
+        if not self.local:
+            import torch.distributed as dist
+            dist.barrier()
+        cur = torch.cuda.current_stream(self.dev)
+        if ev_start is not None:
+            ev_start.record(cur)
+        for r in self.ranks:
+            q = self.per[r]
+            q["stream"].wait_stream(cur)
+            self.shards[r].p2p_launch(q["rp"].data_ptr(), q["nr"], self.recv_bufs[r].data_ptr(), q["sp"].data_ptr(),
+                                      q["speer"].data_ptr(), q["sdst"].data_ptr(), q["ns"], self.peer_recv.data_ptr(),
+                                      self.peer_nrecv.data_ptr(), self.boards[r].data_ptr(),
+                                      self.peer_board.data_ptr(), q["a"].data_ptr(), q["b"].data_ptr(),
+                                      float(threshold), int(max_sweeps), self.ctas, q["ctl"].data_ptr(),
+                                      q["stream"].cuda_stream)
+        for r in self.ranks:
+            cur.wait_stream(self.per[r]["stream"])
+        if ev_end is not None:
+            ev_end.record(cur)
+
+    def collect(self):
+        """After launch() completed: (lam_full in position order, result dict), on every rank."""
+        n, stride, world = self.n, self.stride, self.world
+        lam_full = torch.zeros(stride * world, dtype=torch.float64, device=self.dev)
+        res = None
+        for r in self.ranks:
+            res_r = self._f2m.p2p_result(self.per[r]["ctl"].data_ptr())
+            assert res is None or (res_r["sweeps"], res_r["converged"]) == (res["sweeps"], res["converged"])
+            res = res_r
+            out = self.per[r]["b"] if res_r["out_buffer"] else self.per[r]["a"]
+            lo, hi = r * stride, min((r + 1) * stride, n)
+            lam_full[lo:hi] = out[lo:hi]
+        if not self.local:  # every rank holds its own rows: assemble the full vector
+            mine = lam_full[self.comm.rank * stride:(self.comm.rank + 1) * stride].clone()
+            self.comm.all_gather(lam_full, [mine])
+        return lam_full, res
+
+    def run(self, lam0_full: torch.Tensor, threshold: float, max_sweeps: int):
+        self.launch(lam0_full, threshold, max_sweeps)
+        torch.cuda.synchronize(self.dev)
+        return self.collect()
+
+
+def _solve_duals_p2p(graph, comm, eps, max_sweeps, b, eta, update, init, threshold):
+    from . import _f2m
+
+    if comm is None:
+        comm = TorchDistComm()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sched = ShardedP2P(graph, comm, b, eta, update)
+    n, stride, world = sched.n, sched.stride, sched.world
+    if threshold is None:
+        threshold = eps * graph.mean_cost()  # dual.cpp:221 (host fp64 product, no FMA)
+    lam0 = torch.zeros(stride * world, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if n > 0:
+        _f2m.initial_state_positions(graph, lam0.data_ptr(), b, init, stream)
+    if max_sweeps > 0 and n > 0:
+        lam_full, res = sched.run(lam0, threshold, max_sweeps)
+    else:
+        lam_full, res = lam0, {"converged": False, "sweeps": 0, "final_max_abs_delta": float("inf")}
+    ids = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    if n > 0:
+        _f2m.positions_to_ids(graph, lam_full.data_ptr(), ids.data_ptr(), stream)
+    report = {"converged": res["converged"], "sweeps": res["sweeps"],
+              "final_max_abs_delta": res["final_max_abs_delta"], "world": world, "stride": stride,
+              "exchange": "p2p", "halo_values": sched.halo_values}
+    return ids[:n].cpu().numpy(), report

@@ -285,3 +285,73 @@ def test_nccl_world1_halo_matches_single_gpu():
         assert np.array_equal(lam, np.asarray(st.lam))
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ fused peer-memory solve
+def test_p2p_plan_arrays_match_receive_lists():
+    """Every value a rank sends lands at the index its reader expects for that position."""
+    from paper_2011_08170_b200.sharded import halo_plans, p2p_plan_arrays
+
+    rng = np.random.default_rng(5)
+    n, world = 3000, 5
+    stride = -(-n // world)
+    u = rng.integers(0, n, 20000)
+    v = (u + rng.integers(1, 200, 20000)) % n
+    plans = halo_plans(n, world, stride, u, v)
+    recv = [p2p_plan_arrays(plans, r)[0] for r in range(world)]
+    for q in range(world):
+        _, sp, speer, sdst = p2p_plan_arrays(plans, q)
+        assert np.all(sp // stride == q)  # only own positions are sent
+        for pos, r, d in zip(sp, speer, sdst):
+            assert recv[r][d] == pos
+    assert sum(len(p2p_plan_arrays(plans, q)[1]) for q in range(world)) == sum(len(x) for x in recv)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_local_shards_p2p_match_single_gpu(world):
+    """world concurrent persistent kernels on one GPU exchanging through device memory."""
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_sharded
+
+    g = _gpu_graph(10000, 1)
+    st, rep = f2m.solve_duals(g)
+    lam, srep = solve_duals_sharded(g, LocalComm(world), exchange="p2p")
+    assert srep["sweeps"] == rep["sweeps"] == 3165
+    assert srep["converged"] and rep["converged"]
+    assert srep["final_max_abs_delta"] == rep["final_max_abs_delta"]
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
+def test_local_shards_p2p_truncated_and_fixed_count():
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_sharded
+
+    g = _gpu_graph(5000, 2)
+    st = f2m.make_initial_state(g)
+    f2m.jacobi_sweeps(g, st, 45)
+    lam, srep = solve_duals_sharded(g, LocalComm(4), max_sweeps=45, threshold=-1.0, exchange="p2p")
+    assert srep["sweeps"] == 45 and not srep["converged"]
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
+def test_nccl_world1_p2p_matches_single_gpu():
+    """The multi-process path (torch symmetric memory for the peer buffers) at world 1."""
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import TorchDistComm, solve_duals_sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = _gpu_graph(3000, 4)
+        st, rep = f2m.solve_duals(g)
+        lam, srep = solve_duals_sharded(g, TorchDistComm(), exchange="p2p")
+        assert srep["sweeps"] == rep["sweeps"]
+        assert np.array_equal(lam, np.asarray(st.lam))
+    finally:
+        dist.destroy_process_group()

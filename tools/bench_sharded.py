@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--local", type=int, default=0, help="simulate this many shards in one process")
     ap.add_argument("--solve", action="store_true")
-    ap.add_argument("--exchange", default="halo", choices=["halo", "allgather"])
+    ap.add_argument("--exchange", default="halo", choices=["halo", "allgather", "p2p"])
     args = ap.parse_args()
 
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -42,8 +42,8 @@ def main():
     import torch.distributed as dist
 
     import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200.sharded import (LocalComm, ShardedJacobi, TorchDistComm, make_halo_schedule,
-                                               solve_duals_sharded)
+    from paper_2011_08170_b200.sharded import (LocalComm, ShardedJacobi, ShardedP2P, TorchDistComm,
+                                               make_halo_schedule, solve_duals_sharded)
     from paper_2011_08170_b200 import _f2m
 
     f2m.set_device(local)
@@ -68,6 +68,29 @@ def main():
         if rank == 0:
             st, r1 = f2m.solve_duals(g, max_sweeps=200000)
             line.update(one_gpu_sweeps=r1["sweeps"], bit_identical=bool((lam == st.lam).all()))
+    elif args.exchange == "p2p":  # one persistent kernel per rank for all sweeps (fixed count)
+        stream = torch.cuda.current_stream(dev)
+        sched = ShardedP2P(g, comm)
+        lam0 = torch.zeros(sched.stride * comm.world, dtype=torch.float64, device=dev)
+        _f2m.initial_state_positions(g, lam0.data_ptr(), 2, "local-midpoint", stream.cuda_stream)
+        sched.run(lam0, -1.0, max(args.warmup, 2))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sched.launch(lam0, -1.0, args.sweeps, e0, e1)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if not args.local:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        per = ms * 1e3 / args.sweeps
+        line.update(sweeps=args.sweeps, us_per_sweep=per, gdp_iterations_per_s=1e6 / per,
+                    algorithmic_GBps=g.sweep_bytes() / (per * 1e-6) / 1e9, exchange="p2p",
+                    halo_values_per_sweep=sched.halo_values, ctas_per_rank=sched.ctas)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if not args.local:
+            dist.destroy_process_group()
+        return
     elif args.exchange == "halo":
         stream = torch.cuda.current_stream(dev)
         sched, lam0, meta = make_halo_schedule(g, comm, chunk=args.chunk)
