@@ -233,7 +233,36 @@ def sharded_leg(args, ws, rank, local, dev, n=2_000_000, sweeps=256, chunk=32):
             "algorithmic_GBps": g.sweep_bytes() / (per_us * 1e-6) / 1e9,
             "halo_values_per_sweep": meta["halo_values_per_sweep"],
             "kernel": "k_shard_sweep<2> + halo pack / ncclAllToAll / unpack + chunked ncclAllReduce(max), "
-                      "CUDA-graph replay"}
+                      "CUDA-graph replay"}, g, comm
+
+
+def sharded_p2p_leg(g, comm, dev, sweeps=256):
+    """The same 2M sweeps through the fused peer-memory engine (one persistent kernel per rank,
+    halo and sweep maxima stored into the peers' memory; sharded.ShardedP2P)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import ShardedP2P
+
+    sched = ShardedP2P(g, comm)
+    lam0 = torch.zeros(sched.stride * comm.world, dtype=torch.float64, device=dev)
+    f2m._f2m.initial_state_positions(g, lam0.data_ptr(), 2, "local-midpoint", torch.cuda.current_stream(dev).cuda_stream)
+    sched.run(lam0, -1.0, 8)  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sched.launch(lam0, -1.0, sweeps, e0, e1)
+    torch.cuda.synchronize()
+    lam_full, res = sched.collect()
+    assert res["sweeps"] == sweeps
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    per_us = float(ms.item()) * 1e3 / sweeps
+    return {"workload": f"same as sharded_2m, fused peer-memory engine x{comm.world}",
+            "ranks": comm.world, "us_per_sweep": per_us, "gdp_iterations_per_s": 1e6 / per_us,
+            "algorithmic_GBps": g.sweep_bytes() / (per_us * 1e-6) / 1e9,
+            "halo_values_per_sweep": sched.halo_values,
+            "kernel": f"k_p2p_solve<2> (one persistent launch per rank, {sched.ctas} CTAs x 1024; LL halo stores "
+                      f"into peer memory, per-sweep maxima boards, 2 grid barriers per sweep)"}
 
 
 def run_gpu(args):
@@ -361,8 +390,10 @@ def run_gpu(args):
     # ---- node-sharded engine: the 2M-city instance (BASELINE configs[4]) split
     # across the N ranks, lambda all-gathered with NCCL every sweep; fixed sweep count (the full
     # 2M solve takes tens of thousands of sweeps), device time, max over ranks.
+    sharded_ctx = None
     if not args.no_sharded:
-        line["sharded_2m"] = sharded_leg(args, ws, rank, local, dev)
+        line["sharded_2m"], g2m, comm2m = sharded_leg(args, ws, rank, local, dev)
+        sharded_ctx = (g2m, comm2m)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         sweeps_total = int(sw)
         lam = d_lam.cpu().numpy()
@@ -373,6 +404,11 @@ def run_gpu(args):
                        f"sweeps + extract/verify on the converged lambda, 1 thread; projected to "
                        f"{sweeps_total} sweeps"),
             "detail": detail}
+    if sharded_ctx is not None:  # last: an exchange failure here cannot disturb the legs above
+        try:
+            line["sharded_2m_p2p"] = sharded_p2p_leg(sharded_ctx[0], sharded_ctx[1], dev)
+        except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
+            line["sharded_2m_p2p"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     import torch.distributed as dist
