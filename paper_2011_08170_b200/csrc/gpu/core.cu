@@ -69,7 +69,8 @@ std::shared_ptr<Topology> make_topology(int n, int dev) {
 
 int64_t* pinned_scratch() {
   thread_local int64_t* p = nullptr;
-  if (!p) F2M_CUDA(cudaMallocHost(&p, 64 * sizeof(int64_t)));
+  // portable: the same thread may drive several devices (f2m_set_device)
+  if (!p) F2M_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), 64 * sizeof(int64_t), cudaHostAllocPortable));
   return p;
 }
 
