@@ -1313,8 +1313,10 @@ __global__ void __launch_bounds__(256) k_init_local_midpoint(
 template <int B>
 static void launch_init(const f2m_graph& g, double* d_lam, unsigned long long* ll, int* counter, int* err) {
   const Topology& t = *g.topo;
+  // 4 CTAs (32 warps) per SM: measured 0.14 ms at 100k vs 0.23 ms with 8 (fewer warps spinning
+  // on the id-order frontier, less contention on the claim counter)
   const int blocks = std::max(1, std::min<int>(grid_for((int64_t)t.n * 32, 256),
-                                               device_props(t.dev).multiProcessorCount * 8));
+                                               device_props(t.dev).multiProcessorCount * 4));
   k_init_local_midpoint<B><<<blocks, 256, 0, t.stream>>>(t.n, t.perm.get(), t.iperm.get(), t.deg.get(),
                                                         t.sptr.get(), t.scol.get(), g.scost.get(), d_lam,
                                                         ll, counter, err);
