@@ -397,7 +397,7 @@ struct Sweep4Args {
   const uint8_t* __restrict__ row_nhalo; // v5: halo slots per row
   unsigned poll_ns;          // v5: sync-warp back-off between unproductive halo polls
   int runahead;              // v5: stage the next sweep's halo while this sweep computes
-  int split;                 // v5: scan boundary rows' own-CTA slots before the halo arrives
+  int split;                 // sweep order: 4 boundary rows first (default), 3 same with every warp at the halo hand-off, 1 interior first + own-CTA slots of boundary rows before the halo, 0 interior first
   // deferred threshold (v5): defer_eps > 0 -> threshold = defer_eps * mean_cost, where the master
   // CTA computes mean_cost (sequential sum of cost[0..m) / m, graph.cpp:47-49) during the solve
   double defer_eps;
@@ -636,6 +636,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // boundary row of this thread (per batch of cthreads rows): the rotation starts at the first
   // warp with the fewest interior slices, so boundary work lands on the least-loaded warps
   const int brow = (tid - ((s_int - s_lo) % ncw) * 32 + cthreads) % cthreads;
+  // split == 4: only the warps that own boundary rows (and the sync warps) meet at the halo
+  // hand-off; the others go straight to their interior rows
+  const int halo_bar = (a.split == 4 && nbnd <= cthreads) ? 64 + 32 * ((nbnd + 31) / 32) : cthreads + 64;
+  const bool in_halo_bar = !(a.split == 4 && nbnd <= cthreads) || (brow & ~31) < nbnd;
   const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
   const int64_t slot0 = a.sptr[s_lo];
   const int nslots = (int)(a.sptr[s_hi] - slot0);
@@ -737,13 +741,15 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       if (lane == 0) s_staged[sw] = s;
       // hand-off on a hardware barrier (compute warps sleep in bar.sync, no spinning); two ids
       // alternate so the run-ahead arrival for s+1 can never be counted towards sweep s
-      named_arrive(3 + (s & 1), cthreads + 64);
+      named_arrive(3 + (s & 1), halo_bar);
       if (sw == 0 && lane == 0) s_word = ld_relaxed_u64(&ctl->word);
     }
     return;
   }
 
   // ---- compute warps
+  const bool boundary_first = a.split >= 3;  // boundary rows (whole rows) before the interior
+  const bool split_mode = RES && a.split == 1;
   for (int s = 0;; ++s) {
     if (tid == 0) F2M_TRACE16(s, 0);
     double* lam = (RES && (s & 1)) ? regB : regA;
@@ -755,6 +761,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       named_sync(2, cthreads);
     }
     double mx = 0.0;
+    long long ck0 = 0, ck1 = 0, ck2 = 0, ck3 = 0;
+    double pv[B + 1];
+#pragma unroll
+    for (int i = 0; i <= B; ++i) pv[i] = CUDART_INF;
+    auto interior_rows = [&]() {
     // interior slices: one thread per node (throughput-bound phase)
     for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
       const int p = sl * 32 + lane;
@@ -793,47 +804,16 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       const double ad = fabs(d);
       mx = mx < ad ? ad : mx;
     }
-    if (warp == 0 && lane == 0) F2M_TRACE16(s, 4);
-    // boundary rows, first pass (RES): the own-CTA part of the row while the halo is in flight
-    // (slots are stored own-first, halo-last); the top-(B+1) multiset does not depend on order
-    double pv[B + 1];
-#pragma unroll
-    for (int i = 0; i <= B; ++i) pv[i] = CUDART_INF;
-    if (RES && a.split && brow < nbnd) {
-      const int lp = bstart + brow, p = p0 + lp;
-      const int2 sw2 = slc[(p >> 5) - s_lo];
-      const int lb = sw2.x + (p & 31);
-      const int jo = sw2.y - nh_s[brow];
-      const double lv = lam[lp];
-      for (int jj = 0; jj < jo; jj += 4) {
-        int li[4];
-        double cs[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool ok = jj + u < jo;
-          const int idx = lb + 32 * (ok ? jj + u : 0);
-          li[u] = lid_s[idx];
-          cs[u] = cst_s[idx];
-          if (!ok) {
-            li[u] = lp;
-            cs[u] = CUDART_INF;
-          }
-        }
-        double lu[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) lu[u] = lam[li[u]];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) topk_bubble<B>(pv, dsub(dsub(cs[u], lv), lu[u]));
-      }
-    }
-    named_sync(3 + (s & 1), cthreads + 64);  // halo of sweep s staged
+    };
+    auto halo_and_boundary_rows = [&]() {
+    if (in_halo_bar) named_sync(3 + (s & 1), halo_bar);  // halo of sweep s staged
     if (warp == 0 && lane == 0) {
       F2M_TRACE16(s, 3);
       if (a.trace && s >= a.trace_first && s < a.trace_first + a.trace_count)
         a.trace[(((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4) + 9] =
             (unsigned long long)(long long)(min(s_staged[0], s_staged[1]) - s);
     }
-    long long ck0 = clock64(), ck1 = 0, ck2 = 0, ck3 = 0;
+    ck0 = clock64();
     // boundary rows, second pass: the halo slots (RES, first batch) or the whole row
     {
       unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
@@ -845,7 +825,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           const int2 sw2 = slc[(p >> 5) - s_lo];
           const int lb = sw2.x + (p & 31);
           const int w = sw2.y;
-          const bool split = RES && a.split && base == 0;
+          const bool split = split_mode && base == 0;
           const int j0 = split ? w - nh_s[node] : 0;
           double sv[B + 1];
 #pragma unroll
@@ -893,6 +873,48 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           if (tid == 0 && base == 0) ck3 = clock64();
         }
       }
+    }
+    };
+    if (boundary_first) {
+      // the halo of sweep s was published early in the neighbours' sweep s-1 (they too start
+      // with their boundary rows), so it is normally staged already: publish first, then the
+      // interior rows overlap the neighbours' next exchange
+      halo_and_boundary_rows();
+      interior_rows();
+      if (warp == 0 && lane == 0) F2M_TRACE16(s, 4);
+    } else {
+      interior_rows();
+      if (warp == 0 && lane == 0) F2M_TRACE16(s, 4);
+    // boundary rows, first pass (RES): the own-CTA part of the row while the halo is in flight
+    // (slots are stored own-first, halo-last); the top-(B+1) multiset does not depend on order
+    if (split_mode && brow < nbnd) {
+      const int lp = bstart + brow, p = p0 + lp;
+      const int2 sw2 = slc[(p >> 5) - s_lo];
+      const int lb = sw2.x + (p & 31);
+      const int jo = sw2.y - nh_s[brow];
+      const double lv = lam[lp];
+      for (int jj = 0; jj < jo; jj += 4) {
+        int li[4];
+        double cs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = jj + u < jo;
+          const int idx = lb + 32 * (ok ? jj + u : 0);
+          li[u] = lid_s[idx];
+          cs[u] = cst_s[idx];
+          if (!ok) {
+            li[u] = lp;
+            cs[u] = CUDART_INF;
+          }
+        }
+        double lu[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lu[u] = lam[li[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) topk_bubble<B>(pv, dsub(dsub(cs[u], lv), lu[u]));
+      }
+    }
+      halo_and_boundary_rows();
     }
     if (a.trace && tid == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count) {
       unsigned long long* tr = a.trace + (((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4);
@@ -1152,7 +1174,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.m = t.m;
     a.approx_sum = g.approx_sum.get();
     a.mean_out = mean_out.get();
-    a.split = 1;
+    a.split = 4;  // boundary rows first, only their warps meet at the halo hand-off (1: interior first + split rows)
     if (const char* e = std::getenv("F2M_SPLIT")) a.split = std::atoi(e);
     if (const char* e = std::getenv("F2M_RUNAHEAD")) a.runahead = std::atoi(e);
     if (const char* e = std::getenv("F2M_POLL_NS")) a.poll_ns = (unsigned)std::max(0, std::atoi(e));
