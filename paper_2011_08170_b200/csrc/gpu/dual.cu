@@ -976,10 +976,11 @@ static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t 
   F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
 }
 
-// Resident (smem) layout: 640 threads per CTA (18 compute warps + 2 sync warps, 96 registers):
-// measured best against 512 / 768 / 896 / 1024 — more warps hide more latency until ptxas'
-// register budget (65536 / threads) forces it to serialise each row's load chain. The streaming layout keeps 1024
-// threads for memory-level parallelism.
+// Resident (smem) layout: 768 threads per CTA (22 compute warps + 2 sync warps, 80 registers) with
+// the boundary-first sweep order: at 100k 3.18 us/sweep vs 3.40 (640), 3.48 (832), 3.73 (704),
+// 3.66 (1024) — more warps hide more latency until ptxas' register budget (65536 / threads)
+// serialises each row's load chain (640 was best with the interior-first order). The streaming
+// layout keeps 1024 threads for memory-level parallelism.
 template <bool RES, int NT>
 static void dispatch_sweep5(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
   switch (b) {
@@ -1201,8 +1202,8 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       static int nt = -1;
       if (nt < 0) {
         const char* e = std::getenv("F2M_SWEEP_NT");
-        nt = e ? std::atoi(e) : 640;
-        if (nt != 512 && nt != 768 && nt != 1024) nt = 640;
+        nt = e ? std::atoi(e) : 768;
+        if (nt != 512 && nt != 640 && nt != 1024) nt = 768;
       }
       g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg.b) + (t.resident ? ", resident, " : ", streaming, ") +
                           std::to_string(t.resident ? nt : 1024) + "> (persistent: " + std::to_string(G) +
