@@ -10,6 +10,8 @@
 // (min, max) keys (graph.cpp:223-232); costs are distance(u, v) with no FMA
 // (instance.cpp:134-136). The device node order is the Morton (Z) order of grid cells, which
 // makes a CTA's slice range a compact spatial patch for the sweep's lambda gathers.
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -292,14 +294,35 @@ __device__ __forceinline__ uint64_t spread32(uint32_t v) {
   return x;
 }
 
-__global__ void k_morton(int n, const int32_t* __restrict__ cell_of, const GridParams* __restrict__ gp,
-                         uint64_t* __restrict__ key, int32_t* __restrict__ idx) {
+// Hilbert index of cell (x, y) on a 2^order x 2^order grid (the classic rotate-and-flip walk):
+// consecutive Hilbert ranges are compact patches without Morton's long jumps, so the sweep
+// kernel's CTA partitions have fewer boundary rows and neighbour CTAs.
+__device__ __forceinline__ uint64_t hilbert_d(int order, uint32_t x, uint32_t y) {
+  uint64_t d = 0;
+  for (uint32_t sside = 1u << (order - 1); sside > 0; sside >>= 1) {
+    const uint32_t rx = (x & sside) ? 1u : 0u, ry = (y & sside) ? 1u : 0u;
+    d += (uint64_t)sside * sside * ((3u * rx) ^ ry);
+    if (ry == 0) {  // rotate the quadrant
+      if (rx == 1) {
+        x = sside - 1 - (x & (sside - 1)) + (x & ~(sside - 1));
+        y = sside - 1 - (y & (sside - 1)) + (y & ~(sside - 1));
+      }
+      const uint32_t t = x;
+      x = y;
+      y = t;
+    }
+  }
+  return d;
+}
+
+__global__ void k_morton(int n, const int32_t* __restrict__ cell_of, const GridParams* __restrict__ gp, int order,
+                         int hilbert, uint64_t* __restrict__ key, int32_t* __restrict__ idx) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int c = cell_of[i];
   const int gx = gp->gx;
   const uint32_t cx = (uint32_t)(c % gx), cy = (uint32_t)(c / gx);
-  key[i] = spread32(cx) | (spread32(cy) << 1);
+  key[i] = hilbert ? hilbert_d(order, cx, cy) : (spread32(cx) | (spread32(cy) << 1));
   idx[i] = i;
 }
 
@@ -431,10 +454,15 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
     DBuf<int32_t> i0(n, s);
     t.iperm.alloc(n, s);
     t.perm.alloc(n, s);
-    k_morton<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of.get(), gp.get(), mk0.get(), i0.get());
-    launched("morton");
+    const int order = std::max(bit_width(std::max(hp.gx, hp.gy) - 1), 1);
+    static const int hilbert = [] {
+      const char* e = std::getenv("F2M_ORDER");
+      return (e && e[0] == 'm') ? 0 : 1;  // F2M_ORDER=morton for A/B
+    }();
+    k_morton<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of.get(), gp.get(), order, hilbert, mk0.get(), i0.get());
+    launched("spatial_order");
     size_t tmp = 0;
-    const int mbits = 2 * std::max(bit_width(std::max(hp.gx, hp.gy) - 1), 1);  // interleaved cell coordinates
+    const int mbits = 2 * order;  // both curves index a 2^order x 2^order grid
     F2M_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, mk0.get(), mk1.get(), i0.get(), t.iperm.get(), n,
                                              0, mbits, s));
     DBuf<char> tb(tmp, s);
