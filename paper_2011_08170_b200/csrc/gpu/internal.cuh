@@ -292,14 +292,16 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 // everywhere and falls off the end, as `val < s[b]` rejects it in the reference.
 template <int B>
 __device__ __forceinline__ void topk_bubble(double (&s)[B + 1], double val) {
+  // insertion into the ascending list with all compares against the OLD list (independent, so
+  // they issue back to back): position i takes s[i-1] if val < s[i-1], val if s[i-1] <= val <
+  // s[i], else keeps s[i]. Strict compares: val goes after equal elements, as a sequential
+  // insertion would put it.
+  bool c[B + 1];
 #pragma unroll
-  for (int i = 0; i < B; ++i) {
-    const bool lt = val < s[i];
-    const double lo = lt ? val : s[i];
-    val = lt ? s[i] : val;
-    s[i] = lo;
-  }
-  s[B] = val < s[B] ? val : s[B];
+  for (int i = 0; i <= B; ++i) c[i] = val < s[i];
+#pragma unroll
+  for (int i = B; i > 0; --i) s[i] = c[i - 1] ? s[i - 1] : (c[i] ? val : s[i]);
+  s[0] = c[0] ? val : s[0];
 }
 
 __device__ __forceinline__ uint64_t splitmix64_at(uint64_t state0, uint64_t draw_index) {
