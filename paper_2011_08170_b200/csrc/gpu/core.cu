@@ -559,13 +559,12 @@ static void build_local_index(Topology& t) {
     k_local_sizes<<<grid_for(G, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.halo_off.get(), t.sptr.get(), ml.get(),
                                                    ms.get());
     launched("local_sizes");
-    int hml = 0;
-    unsigned long long hms = 0;
-    F2M_CUDA(cudaMemcpyAsync(&hml, ml.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaMemcpyAsync(&hms, ms.get(), sizeof(hms), cudaMemcpyDeviceToHost, s));
+    int64_t* hs = pinned_scratch();  // both sizes with one synchronisation
+    F2M_CUDA(cudaMemcpyAsync(hs + 1, ml.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 2, ms.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
-    t.max_local = hml;
-    t.max_cta_slots = (int64_t)hms;
+    t.max_local = *reinterpret_cast<const int*>(hs + 1);
+    t.max_cta_slots = hs[2];
   }
   const size_t limit = sweep_smem_limit(t.dev);
   const size_t lam_bytes = (size_t)t.max_local * sizeof(double);

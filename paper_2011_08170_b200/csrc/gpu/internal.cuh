@@ -195,7 +195,7 @@ __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return
 // scalars are queued asynchronously into it and collected with ONE stream synchronisation
 // (a D2H copy into pageable memory is itself synchronous). 64 int64 slots: 0-15 topology
 // build, 20 init watchdog, 24 dual objective, 26-28 certification, 32-47 sweep control
-// block, 48 deferred mean.
+// block, 48 deferred mean, 50-57 k-NN grid parameters, 58 k-NN edge count.
 int64_t* pinned_scratch();
 
 // number of bits needed to represent v >= 0 (0 -> 0)

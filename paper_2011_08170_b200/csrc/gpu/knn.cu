@@ -11,6 +11,7 @@
 // (instance.cpp:134-136). The device node order is the Morton (Z) order of grid cells, which
 // makes a CTA's slice range a compact spatial patch for the sweep's lambda gathers.
 #include <cstdlib>
+#include <cstring>
 
 #include <cub/cub.cuh>
 
@@ -369,8 +370,10 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   k_grid_params<<<1, 1, 0, s>>>(n, acc.get(), gp.get());
   launched("grid_params");
   GridParams hp;
-  F2M_CUDA(cudaMemcpyAsync(&hp, gp.get(), sizeof(hp), cudaMemcpyDeviceToHost, s));
+  static_assert(sizeof(GridParams) <= 8 * sizeof(int64_t), "pinned scratch slots 50-57");
+  F2M_CUDA(cudaMemcpyAsync(pinned_scratch() + 50, gp.get(), sizeof(hp), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(&hp, pinned_scratch() + 50, sizeof(hp));
   const int64_t cells = (int64_t)hp.gx * hp.gy;
   DBuf<int32_t> cell_of(n, s), cnt(cells + 1, s), off(cells + 1, s), cur(cells, s), ids(n, s);
   DBuf<double2> pts(n, s);
@@ -438,8 +441,9 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
     launched("unique_pairs");
   }
   int64_t m = 0;
-  F2M_CUDA(cudaMemcpyAsync(&m, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  F2M_CUDA(cudaMemcpyAsync(pinned_scratch() + 58, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
+  m = pinned_scratch()[58];
   t.m = m;
   t.eu.alloc(m, s);
   t.ev.alloc(m, s);
