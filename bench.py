@@ -9,7 +9,8 @@ generator), i.e. the reference's full_solve (solve.cpp:101-106).
   value      device time per solve with the points already resident in HBM and x / lambda
              left in HBM (CUDA events on the solve's stream), via f2m_full_solve_device.
   e2e        the same solve through the public C ABI with host buffers (f2m_full_solve via the
-             pybind module): pinned host points -> device, x and lambda -> host, wall clock.
+             pybind module): pinned host points -> device, x and lambda -> caller-owned pinned
+             host buffers, wall clock.
   roofline   the dominant kernel, the persistent GDP sweep kernel: algorithmic bytes per launch
              (4(n+1) + 2m*12 + 16n per sweep, times the sweeps of the launch)
              over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
@@ -22,7 +23,8 @@ Multi-GPU (torchrun, N>1): every rank solves its own replica of the headline ins
 scaling, no data-path collective): that is `value`. The line also carries `sharded_2m`: the
 node-sharded engine on the 2M-city instance split across the N ranks (halo
 exchange of the multipliers other ranks read, NCCL all-to-all per sweep), per-sweep device time
-over a fixed sweep count.
+over a fixed sweep count, and `sharded_2m_p2p`: the same sweeps through the fused peer-memory
+engine (one persistent kernel per rank; reported as unavailable if peer memory cannot be set up).
 """
 from __future__ import annotations
 
