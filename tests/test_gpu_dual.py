@@ -258,6 +258,59 @@ def test_grid_barrier_kernel_fallback_parity():
     assert sweeps == meta["sweeps"] and dual == meta["dual_value"] and digest == meta["sha256"]["lam_final"]
 
 
+def _run_sub(code, env):
+    import os
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return out.stdout.strip().splitlines()[-1]
+
+
+@pytest.mark.parametrize("order", ["0", "1", "3", "4", "6"])
+def test_sweep_orders_bit_exact(order):
+    """Every sweep order of the persistent kernel (interior first with / without split rows,
+    boundary first with all / only boundary warps at the halo hand-off, boundary pairs) gives
+    the reference's trajectory on the 10k golden instance."""
+    import json
+    import os
+    from conftest import ROOT
+    code = (
+        "import sys, json, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2011_08170_b200 as f2m\n"
+        "g = f2m.build_knn_graph(f2m.generate_instance(10000, 1, 1000.0), 10)\n"
+        "st, rep = f2m.solve_duals(g)\n"
+        "print(json.dumps([rep['sweeps'], rep['dual_value'], hashlib.sha256(np.array(st.lam).tobytes()).hexdigest(),"
+        " f2m.last_sweep_kernel_desc()]))\n"
+    ) % (ROOT,)
+    sweeps, dual, digest, desc = json.loads(_run_sub(code, {"F2M_SPLIT": order}))
+    meta, _ = golden("u10k_s1")
+    assert "k_gdp_sweep5" in desc
+    assert sweeps == meta["sweeps"] and dual == meta["dual_value"] and digest == meta["sha256"]["lam_final"]
+
+
+def test_streaming_kernel_matches_grid_barrier_kernel():
+    """A graph too large for shared-memory residency (400k cities) runs the streaming form of the
+    persistent kernel; its multipliers and per-sweep maxima equal the grid-barrier kernel's."""
+    import json
+    import os
+    from conftest import ROOT
+    code = (
+        "import sys, json, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2011_08170_b200 as f2m\n"
+        "g = f2m.build_knn_graph(f2m.generate_instance(400000, 3, 1000.0), 10)\n"
+        "st = f2m.make_initial_state(g)\n"
+        "rec, dv = f2m.jacobi_sweeps(g, st, 300)\n"
+        "print(json.dumps([hashlib.sha256(np.array(st.lam).tobytes()).hexdigest(),"
+        " hashlib.sha256(np.asarray(rec).tobytes()).hexdigest(), dv, f2m.last_sweep_kernel_desc()]))\n"
+    ) % (ROOT,)
+    a = json.loads(_run_sub(code, {}))
+    b = json.loads(_run_sub(code, {"F2M_SWEEP_V1": "1"}))
+    assert "streaming" in a[3] and "k_gdp_sweep<" in b[3]
+    assert a[:3] == b[:3]
+
+
 # ------------------------------------------------------------------ all-pairs (complete graphs)
 @pytest.mark.parametrize("n,seed,rounded", [(8, 1, False), (60, 2, False), (300, 3, True), (1200, 4, False)])
 def test_allpairs_complete_graph_matches_oracle(f2m, n, seed, rounded):
