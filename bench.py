@@ -24,7 +24,8 @@ scaling, no data-path collective): that is `value`. The line also carries `shard
 node-sharded engine on the 2M-city instance split across the N ranks (halo
 exchange of the multipliers other ranks read, NCCL all-to-all per sweep), per-sweep device time
 over a fixed sweep count, and `sharded_2m_p2p`: the same sweeps through the fused peer-memory
-engine (one persistent kernel per rank; reported as unavailable if peer memory cannot be set up).
+engine (one persistent kernel per rank; reported as unavailable if peer memory cannot be set up;
+with N > 1 only when F2M_BENCH_P2P=1).
 """
 from __future__ import annotations
 
@@ -406,7 +407,10 @@ def run_gpu(args):
                        f"sweeps + extract/verify on the converged lambda, 1 thread; projected to "
                        f"{sweeps_total} sweeps"),
             "detail": detail}
-    if sharded_ctx is not None:  # last: an exchange failure here cannot disturb the legs above
+    # last: an exchange failure here cannot disturb the legs above. Across processes the peer
+    # buffers need a collective rendezvous (torch symmetric memory); a rank that failed before it
+    # would leave the others waiting, so N > 1 runs it only on request (F2M_BENCH_P2P=1)
+    if sharded_ctx is not None and (ws == 1 or os.environ.get("F2M_BENCH_P2P") == "1"):
         try:
             line["sharded_2m_p2p"] = sharded_p2p_leg(sharded_ctx[0], sharded_ctx[1], dev)
         except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
