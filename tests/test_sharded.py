@@ -355,3 +355,26 @@ def test_nccl_world1_p2p_matches_single_gpu():
         assert np.array_equal(lam, np.asarray(st.lam))
     finally:
         dist.destroy_process_group()
+
+
+def test_p2p_plan_arrays_degenerate_worlds():
+    """World 1 (nothing crosses) and a rank that owns no row of any cross edge."""
+    from paper_2011_08170_b200.sharded import halo_plans, p2p_plan_arrays
+
+    u = np.array([0, 1, 2, 3], np.int64)
+    v = np.array([1, 2, 3, 0], np.int64)
+    plans = halo_plans(4, 1, 4, u, v)
+    rp, sp, speer, sdst = p2p_plan_arrays(plans, 0)
+    assert len(rp) == len(sp) == len(speer) == len(sdst) == 0
+    # world 3 over 6 positions, edges only inside rank 0 and between ranks 1 and 2
+    u = np.array([0, 2, 3], np.int64)
+    v = np.array([1, 4, 5], np.int64)
+    plans = halo_plans(6, 3, 2, u, v)
+    rp0, sp0, _, _ = p2p_plan_arrays(plans, 0)
+    assert len(rp0) == 0 and len(sp0) == 0
+    rp1, sp1, speer1, sdst1 = p2p_plan_arrays(plans, 1)
+    rp2, sp2, speer2, sdst2 = p2p_plan_arrays(plans, 2)
+    assert sorted(rp1.tolist()) == [4, 5] and sorted(rp2.tolist()) == [2, 3]
+    for sp, speer, sdst in ((sp1, speer1, sdst1), (sp2, speer2, sdst2)):
+        for pos, r, d in zip(sp, speer, sdst):
+            assert [rp1, rp2][r - 1][d] == pos
