@@ -322,6 +322,23 @@ int f2m_p2p_launch(const f2m_shard* s, const f2m_engine_config* cfg, const f2m_p
                    double* d_lam_b, double threshold, int max_sweeps, int ctas, void* d_ctl, void* stream);
 int f2m_p2p_get_result(const void* d_ctl, f2m_p2p_result* out);
 
+/* ---- multi-GPU partition-resident sweep (the one-GPU persistent kernel across ranks) ---------
+ * Build the (replicated) graph after f2m_set_sweep_partition(world * Gp); rank r then runs
+ * partition CTAs [r*Gp, (r+1)*Gp) + its own convergence master. d_ring: kLamBufs (8) x n doubles,
+ * buffer 0 = lambda_0 (full, position order); d_ll / d_cmax: this rank's LL and max rings (sizes
+ * from f2m_sweep_multi_info, zeroed on every rank before any launch), d_*_peers: device arrays of
+ * every rank's ring (peer memory). Asynchronous; f2m_sweep_multi_result after the stream
+ * completes: lambda_{k+1} of positions [begin, end) is in ring buffer out_buffer. */
+void f2m_set_sweep_partition(int ctas);
+int f2m_sweep_multi_info(const f2m_graph* g, int rank, int world, int* g_total, int* resident, int64_t* ll_words,
+                         int64_t* cmax_words, int* begin, int* end);
+size_t f2m_sweep_multi_ctl_bytes(void);
+int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_config* cfg, int rank, int world, double* d_ring,
+                           unsigned long long* d_ll, unsigned long long* const* d_ll_peers,
+                           unsigned long long* d_cmax, unsigned long long* const* d_cmax_peers, double threshold,
+                           int max_sweeps, void* d_ctl, void* stream);
+int f2m_sweep_multi_result(const void* d_ctl, int* sweeps, int* converged, double* final_max, int* out_buffer);
+
 /* ---- instrumentation (bench.py / tests) ----------------------------------------------- */
 /* Number of kernels this library launched since load (all entry points). */
 uint64_t f2m_kernel_launch_count(void);

@@ -67,6 +67,10 @@ std::shared_ptr<Topology> make_topology(int n, int dev) {
 
 // ---------------------------------------------------------------- kernels
 
+// partition CTA count for graphs built from now on (0: one per SM but one); the multi-GPU sweep
+// partitions a replicated graph into world x (SMs - 1) CTAs
+int g_sweep_partition = 0;
+
 int64_t* pinned_scratch() {
   thread_local int64_t* p = nullptr;
   // portable: the same thread may drive several devices (f2m_set_device)
@@ -659,7 +663,7 @@ static void build_local_index(Topology& t) {
   // sweeps from its next verdict on, so a slot is rewritten (sweep k+64) only long after the master
   // has consumed it (window end <= verdict + 16 < k + 56): the ring is race-free for any G. The
   // grid itself is one CTA per SM (G + master <= SM count); 256 bounds the partition tables.
-  if (G > 256) return;  // v1 kernel
+  if (G > 4096) return;  // v1 kernel
   t.v2 = true;
   t.resident = resident_bytes <= limit;
   t.smem_bytes = t.resident ? resident_bytes : streaming_bytes;
@@ -682,7 +686,8 @@ void finalize_topology(Topology& t) {
   t.nslices = (n + 31) / 32;
   // one SM stays free for the v5 kernel's convergence-master CTA
   const int sms = sweep_grid_ctas(t.dev);
-  t.sweep_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms > 1 ? sms - 1 : 1, t.nslices));
+  const int target = g_sweep_partition > 0 ? g_sweep_partition : (sms > 1 ? sms - 1 : 1);
+  t.sweep_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(target, t.nslices));
   const int G = t.sweep_ctas;
   t.cta_lo.alloc(G + 1, s);
   t.cta_int_hi.alloc(G, s);
@@ -1089,3 +1094,6 @@ extern "C" double f2m_sweep_algorithmic_bytes(const f2m_graph* g) {
   const Topology& t = *g->topo;
   return 4.0 * (t.n + 1) + 2.0 * t.m * 12.0 + 16.0 * t.n;
 }
+
+
+extern "C" void f2m_set_sweep_partition(int ctas) { f2mgpu::g_sweep_partition = ctas > 0 ? ctas : 0; }

@@ -407,6 +407,14 @@ struct Sweep4Args {
   double* mean_out;
   unsigned long long* trace;
   int trace_first, trace_count;
+  // multi-GPU form (npeers > 0): this launch runs partition CTAs [cta_base, cta_base + gridDim.x -
+  // 1) of g_total; every boundary multiplier and every CTA's sweep max is stored into all peers'
+  // LL / max rings (peer memory), so each rank's master sees every CTA and issues the same verdicts
+  int cta_base;
+  int g_total;
+  int npeers;
+  unsigned long long* const* ll_peers;
+  unsigned long long* const* cmax_peers;
 };
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
@@ -606,6 +614,32 @@ __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__
   }
 }
 
+__device__ __forceinline__ void st_ll_sys(unsigned long long* p, double v, unsigned tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long hi = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(hi | (b & 0xffffffffull)),
+               "l"(hi | (b >> 32))
+               : "memory");
+}
+
+// LL stores of the sweep kernel; in the multi-GPU form into every rank's ring (same offset,
+// system scope: the readers are on other GPUs)
+__device__ __forceinline__ void publish_ll(const Sweep4Args& a, unsigned long long* local, double v, unsigned tag) {
+  if (!a.npeers) {
+    st_ll(local, v, tag);
+    return;
+  }
+  const size_t off = (size_t)(local - a.ll);
+  for (int q = 0; q < a.npeers; ++q) st_ll_sys(a.ll_peers[q] + off, v, tag);
+}
+__device__ __forceinline__ void publish_cmax(const Sweep4Args& a, size_t off, double v, unsigned tag) {
+  if (!a.npeers) {
+    st_ll(a.cmax + off, v, tag);
+    return;
+  }
+  for (int q = 0; q < a.npeers; ++q) st_ll_sys(a.cmax_peers[q] + off, v, tag);
+}
+
 template <int B, bool RES, int NT>
 __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -616,11 +650,13 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   __shared__ volatile int s_dummy;
   __shared__ volatile int s_staged[2];
   __shared__ unsigned long long s_word;
-  // CTAs 0..G-1 own the partition; CTA G (alone on its SM) is the convergence master
-  const int c = blockIdx.x, G = gridDim.x - 1;
+  // CTAs 0..G-1 own the partition; the last CTA of the launch (alone on its SM) is the master.
+  // Multi-GPU: this launch's CTAs are the partition CTAs cta_base.. of g_total.
+  const int G = a.npeers ? a.g_total : (int)gridDim.x - 1;
+  const int c = (int)blockIdx.x + (a.npeers ? a.cta_base : 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int sync0 = nwarps - 2, ncw = nwarps - 2;
-  if (c == G) {
+  if (blockIdx.x == gridDim.x - 1) {
     sweep_master(a.cmax, a.max_sweeps, a.threshold, a.record, a.trace, a.trace_first, a.trace_count, ctl, G,
                  a.defer_eps, a.cost, a.m, a.approx_sum, a.mean_out);
     return;
@@ -865,7 +901,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         if (node < nbnd && half == 0) {
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          if (lp >= nint) publish_ll(a, llout + 2 * (bo + lp), nl, (unsigned)s + 1);
           gout[p] = nl;
           lam_next[lp] = nl;
           const double ad = fabs(d);
@@ -919,7 +955,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           }
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (lp >= nint) st_ll(llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          if (lp >= nint) publish_ll(a, llout + 2 * (bo + lp), nl, (unsigned)s + 1);
           gout[p] = nl;
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
@@ -1015,7 +1051,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     if (warp == ncw - 1) {  // the CTA max goes out from the warp with the least boundary work
       const unsigned long long bm = warp_max_nonneg(lane < ncw ? red[s & 1][lane] : 0.0);
       if (lane == 0) {
-        st_ll(a.cmax + ((size_t)(s % kCmaxRing) * G + c) * 2, __longlong_as_double((long long)bm), (unsigned)s + 1);
+        publish_cmax(a, ((size_t)(s % kCmaxRing) * G + c) * 2, __longlong_as_double((long long)bm), (unsigned)s + 1);
         s_done = s + 1;
         F2M_TRACE16(s, 6);
       }
@@ -1247,6 +1283,11 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.record = d_record;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
     a.trace = nullptr;
+    a.cta_base = 0;
+    a.g_total = G;
+    a.npeers = 0;
+    a.ll_peers = nullptr;
+    a.cmax_peers = nullptr;
     a.trace_first = a.trace_count = 0;
     DBuf<unsigned long long> trace;
     if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {
@@ -1769,4 +1810,108 @@ extern "C" int f2m_last_sweep_kernel_ms(double* ms, int* sweeps) {
   if (ms) *ms = g_last_sweep_ms;
   if (sweeps) *sweeps = g_last_sweep_count;
   return F2M_OK;
+}
+
+
+// ---------------------------------------------------------------- multi-GPU persistent sweep
+// The partition-resident sweep kernel spread over `world` ranks: the graph (identical on every
+// rank) is partitioned into g_total = world x Gp CTAs (f2m_set_sweep_partition before building
+// it); rank r launches CTAs [r*Gp, (r+1)*Gp) plus its own master. LL and max rings are stored
+// into every rank's copy (peer memory), so every master issues the same verdicts.
+extern "C" int f2m_sweep_multi_info(const f2m_graph* g, int rank, int world, int* g_total, int* resident,
+                                    int64_t* ll_words, int64_t* cmax_words, int* begin, int* end) {
+  return f2mgpu::guard([&] {
+    using namespace f2mgpu;
+    const Topology& t = *g->topo;
+    if (!t.v2) throw Error(F2M_E_ARGUMENT, "multi sweep: the graph has no partition-resident layout");
+    if (world < 1 || t.sweep_ctas % world) throw Error(F2M_E_ARGUMENT, "multi sweep: partition not divisible by world");
+    const int G = t.sweep_ctas, Gp = G / world;
+    *g_total = G;
+    *resident = t.resident ? 1 : 0;
+    *ll_words = (int64_t)kLLRing * std::max(t.nboundary, 1) * 2;
+    *cmax_words = (int64_t)kCmaxRing * G * 2;
+    int32_t lo[2];
+    F2M_CUDA(cudaMemcpy(&lo[0], t.cta_lo.get() + rank * Gp, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    F2M_CUDA(cudaMemcpy(&lo[1], t.cta_lo.get() + (rank + 1) * Gp, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    *begin = std::min(lo[0] * 32, t.n);
+    *end = std::min(lo[1] * 32, t.n);
+  });
+}
+
+extern "C" size_t f2m_sweep_multi_ctl_bytes(void) { return sizeof(f2mgpu::Sweep4Ctl); }
+
+extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_config* cfg, int rank, int world,
+                                      double* d_ring, unsigned long long* d_ll,
+                                      unsigned long long* const* d_ll_peers, unsigned long long* d_cmax,
+                                      unsigned long long* const* d_cmax_peers, double threshold, int max_sweeps,
+                                      void* d_ctl, void* stream) {
+  return f2mgpu::guard([&] {
+    using namespace f2mgpu;
+    validate_engine(*cfg);
+    const Topology& t = *g->topo;
+    if (!t.v2 || t.sweep_ctas % world) throw Error(F2M_E_ARGUMENT, "multi sweep: bad partition");
+    if (t.n > 0 && t.min_deg <= cfg->b)
+      throw Error(F2M_E_DEGREE, "node has degree " + std::to_string(t.min_deg) + " <= b = " + std::to_string(cfg->b));
+    const int G = t.sweep_ctas, Gp = G / world;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Sweep4Ctl* ctl = static_cast<Sweep4Ctl*>(d_ctl);
+    F2M_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Sweep4Ctl), s));
+    Sweep4Args a{};
+    a.n = t.n;
+    a.sptr = t.sptr.get();
+    a.swidth = t.swidth.get();
+    a.cta_lo = t.cta_lo.get();
+    a.cta_int_hi = t.cta_int_hi.get();
+    a.cta_nint = t.cta_nint.get();
+    a.boff = t.boff.get();
+    a.slidx = t.slidx.get();
+    a.scost = g->scost.get();
+    a.halo_off = t.halo_off.get();
+    a.halo = t.halo.get();
+    a.halo_pub = t.halo_pub.get();
+    a.gl = d_ring;  // kLamBufs x n; buffer 0 holds lambda_0 (full vector) on entry
+    a.gstride = (size_t)std::max(t.n, 1);
+    a.ll = d_ll;
+    a.nb = std::max(t.nboundary, 1);
+    a.sdest = t.sdest.get();
+    a.row_nhalo = t.row_nhalo.get();
+    a.poll_ns = 64;
+    a.runahead = 1;
+    a.defer_eps = 0.0;
+    a.cost = g->cost.get();
+    a.m = t.m;
+    a.approx_sum = g->approx_sum.get();
+    a.mean_out = nullptr;
+    a.split = t.n <= 256 * G ? 6 : 4;
+    a.cmax = d_cmax;
+    a.eta = cfg->eta;
+    a.update = cfg->update;
+    a.threshold = threshold;
+    a.max_sweeps = max_sweeps;
+    a.record = nullptr;
+    a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.trace = nullptr;
+    a.trace_first = a.trace_count = 0;
+    a.cta_base = rank * Gp;
+    a.g_total = G;
+    a.npeers = world;
+    a.ll_peers = d_ll_peers;
+    a.cmax_peers = d_cmax_peers;
+    if (t.resident) dispatch_sweep5<true, 768>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
+    else dispatch_sweep5<false, 1024>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
+    launched("gdp_sweep5_multi");
+  });
+}
+
+extern "C" int f2m_sweep_multi_result(const void* d_ctl, int* sweeps, int* converged, double* final_max,
+                                      int* out_buffer) {
+  return f2mgpu::guard([&] {
+    f2mgpu::Sweep4Ctl h;
+    F2M_CUDA(cudaMemcpy(&h, d_ctl, sizeof(h), cudaMemcpyDeviceToHost));
+    if (h.abort) throw f2mgpu::Error(F2M_E_TIMEOUT, "multi sweep: synchronisation watchdog fired");
+    *sweeps = h.sweeps;
+    *converged = h.converged;
+    *final_max = h.final_max;
+    *out_buffer = h.out_buffer;
+  });
 }

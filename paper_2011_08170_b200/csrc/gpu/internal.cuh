@@ -197,6 +197,7 @@ __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return
 // build, 20 init watchdog, 24 dual objective, 26-28 certification, 32-47 sweep control
 // block, 48 deferred mean, 50-57 k-NN grid parameters, 58 k-NN edge count.
 int64_t* pinned_scratch();
+extern int g_sweep_partition;  // f2m_set_sweep_partition
 
 // number of bits needed to represent v >= 0 (0 -> 0)
 inline int bit_width(int64_t v) {

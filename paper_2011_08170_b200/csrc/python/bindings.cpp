@@ -470,6 +470,43 @@ PYBIND11_MODULE(_f2m, m) {
            py::arg("send_dst"), py::arg("n_send"), py::arg("peer_recv"), py::arg("peer_nrecv"), py::arg("board"),
            py::arg("peer_board"), py::arg("lam_a"), py::arg("lam_b"), py::arg("threshold"), py::arg("max_sweeps"),
            py::arg("ctas"), py::arg("ctl"), py::arg("stream") = 0);
+  m.def("set_sweep_partition", [](int ctas) { f2m_set_sweep_partition(ctas); }, py::arg("ctas"));
+  m.def("sweep_multi_info", [](const f2m::Graph& graph, int rank, int world) {
+    int gt = 0, res = 0, b = 0, e = 0;
+    std::int64_t llw = 0, cmw = 0;
+    f2m::check(f2m_sweep_multi_info(graph.handle(), rank, world, &gt, &res, &llw, &cmw, &b, &e));
+    return py::dict(py::arg("g_total") = gt, py::arg("resident") = (bool)res, py::arg("ll_words") = llw,
+                    py::arg("cmax_words") = cmw, py::arg("begin") = b, py::arg("end") = e);
+  });
+  m.def("sweep_multi_ctl_bytes", []() { return f2m_sweep_multi_ctl_bytes(); });
+  m.def(
+      "sweep_multi_launch",
+      [](const f2m::Graph& graph, int b, double eta, const std::string& update, int rank, int world,
+         std::uintptr_t ring, std::uintptr_t ll, std::uintptr_t ll_peers, std::uintptr_t cmax,
+         std::uintptr_t cmax_peers, double threshold, int max_sweeps, std::uintptr_t ctl, std::uintptr_t stream) {
+        f2m_engine_config c{};
+        c.b = b;
+        c.eta = eta;
+        c.eps = 1e-9;
+        c.max_sweeps = max_sweeps;
+        c.update = update == "paper-difference" ? 1 : 0;
+        f2m::check(f2m_sweep_multi_launch(graph.handle(), &c, rank, world, reinterpret_cast<double*>(ring),
+                                          reinterpret_cast<unsigned long long*>(ll),
+                                          reinterpret_cast<unsigned long long* const*>(ll_peers),
+                                          reinterpret_cast<unsigned long long*>(cmax),
+                                          reinterpret_cast<unsigned long long* const*>(cmax_peers), threshold,
+                                          max_sweeps, reinterpret_cast<void*>(ctl), reinterpret_cast<void*>(stream)));
+      },
+      py::arg("graph"), py::arg("b"), py::arg("eta"), py::arg("update"), py::arg("rank"), py::arg("world"),
+      py::arg("ring"), py::arg("ll"), py::arg("ll_peers"), py::arg("cmax"), py::arg("cmax_peers"),
+      py::arg("threshold"), py::arg("max_sweeps"), py::arg("ctl"), py::arg("stream") = 0);
+  m.def("sweep_multi_result", [](std::uintptr_t ctl) {
+    int sw = 0, conv = 0, ob = 0;
+    double fm = 0.0;
+    f2m::check(f2m_sweep_multi_result(reinterpret_cast<const void*>(ctl), &sw, &conv, &fm, &ob));
+    return py::dict(py::arg("sweeps") = sw, py::arg("converged") = (bool)conv, py::arg("final_max_abs_delta") = fm,
+                    py::arg("out_buffer") = ob);
+  });
   m.def("p2p_ctl_bytes", []() { return f2m_p2p_ctl_bytes(); });
   m.def("p2p_max_ctas", [](int b) {
     const int v = f2m_p2p_max_ctas(b);

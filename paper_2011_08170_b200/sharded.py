@@ -578,3 +578,136 @@ def _solve_duals_p2p(graph, comm, eps, max_sweeps, b, eta, update, init, thresho
               "final_max_abs_delta": res["final_max_abs_delta"], "world": world, "stride": stride,
               "exchange": "p2p", "halo_values": sched.halo_values}
     return ids[:n].cpu().numpy(), report
+
+
+class ShardedResident:
+    """The one-GPU partition-resident sweep kernel (k_gdp_sweep5) spread over ranks: the graph is
+    built once per rank with world x Gp partition CTAs (f2m_set_sweep_partition), rank r runs CTAs
+    [r*Gp, (r+1)*Gp) plus its own convergence master, and every boundary multiplier and CTA sweep
+    max is stored into every rank's LL / max ring (NVLink peer memory via torch symmetric memory;
+    plain device memory for LocalComm ranks, which then run concurrently on one GPU). No barrier,
+    host work or collective per sweep; bit-identical to one GPU.
+
+    ShardedResident(inst, k, comm).run(threshold, max_sweeps) -> (lambda in node-id order, report)."""
+
+    def __init__(self, inst, k: int, comm, b: int = 2, eta: float = 0.5, update: str = "midpoint",
+                 init: str = "local-midpoint", ctas_per_rank: int = 0):
+        import paper_2011_08170_b200 as f2m
+        from . import _f2m
+
+        self._f2m = _f2m
+        self.comm = comm
+        self.b, self.eta, self.update = b, eta, update
+        self.dev = dev = torch.device("cuda", torch.cuda.current_device())
+        self.world = world = comm.world
+        self.local = local = not isinstance(comm, TorchDistComm)
+        self.ranks = list(range(world)) if local else [comm.rank]
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        # one SM per rank's master; in-process ranks share this device's SMs
+        gp = ctas_per_rank or (max(1, (sms - world) // world) if local else sms - 1)
+        _f2m.set_sweep_partition(world * gp)
+        try:
+            self.graph = f2m.build_knn_graph(inst, k)
+        finally:
+            _f2m.set_sweep_partition(0)
+        g = self.graph
+        self.n = n = g.n
+        self.info = {r: _f2m.sweep_multi_info(g, r, world) for r in self.ranks}
+        i0 = next(iter(self.info.values()))
+        self.g_total = i0["g_total"]
+        llw, cmw = int(i0["ll_words"]), int(i0["cmax_words"])
+        if local:
+            self.ll = {r: torch.zeros(llw, dtype=torch.int64, device=dev) for r in self.ranks}
+            self.cmax = {r: torch.zeros(cmw, dtype=torch.int64, device=dev) for r in self.ranks}
+            ll_ptrs = [self.ll[r].data_ptr() for r in range(world)]
+            cm_ptrs = [self.cmax[r].data_ptr() for r in range(world)]
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            group = comm.group if comm.group is not None else dist.group.WORLD
+            lb = symm_mem.empty(llw, dtype=torch.int64, device=dev)
+            cb = symm_mem.empty(cmw, dtype=torch.int64, device=dev)
+            self._handles = (symm_mem.rendezvous(lb, group), symm_mem.rendezvous(cb, group))
+            self.ll, self.cmax = {comm.rank: lb}, {comm.rank: cb}
+            ll_ptrs, cm_ptrs = list(self._handles[0].buffer_ptrs), list(self._handles[1].buffer_ptrs)
+        self.ll_peers = torch.tensor(ll_ptrs, dtype=torch.int64, device=dev)
+        self.cmax_peers = torch.tensor(cm_ptrs, dtype=torch.int64, device=dev)
+        self.lam0 = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        if n > 0:
+            _f2m.initial_state_positions(g, self.lam0.data_ptr(), b, init, torch.cuda.current_stream(dev).cuda_stream)
+        self.rings = {r: torch.empty((8, max(n, 1)), dtype=torch.float64, device=dev) for r in self.ranks}
+        self.ctl = {r: torch.zeros(_f2m.sweep_multi_ctl_bytes() // 8 + 1, dtype=torch.int64, device=dev)
+                    for r in self.ranks}
+        self.streams = {r: torch.cuda.Stream(dev) for r in self.ranks}
+
+    def launch(self, threshold: float, max_sweeps: int, ev_start=None, ev_end=None) -> None:
+        for r in self.ranks:
+            self.ll[r].zero_()
+            self.cmax[r].zero_()
+            self.rings[r][0].copy_(self.lam0)
+        torch.cuda.synchronize(self.dev)  # rings zeroed on every rank before any rank publishes
+        if not self.local:
+            import torch.distributed as dist
+            dist.barrier()
+        cur = torch.cuda.current_stream(self.dev)
+        if ev_start is not None:
+            ev_start.record(cur)
+        for r in self.ranks:
+            st = self.streams[r]
+            st.wait_stream(cur)
+            self._f2m.sweep_multi_launch(self.graph, self.b, self.eta, self.update, r, self.world,
+                                         self.rings[r].data_ptr(), self.ll[r].data_ptr(), self.ll_peers.data_ptr(),
+                                         self.cmax[r].data_ptr(), self.cmax_peers.data_ptr(), float(threshold),
+                                         int(max_sweeps), self.ctl[r].data_ptr(), st.cuda_stream)
+        for r in self.ranks:
+            cur.wait_stream(self.streams[r])
+        if ev_end is not None:
+            ev_end.record(cur)
+
+    def collect(self):
+        n = self.n
+        lam_pos = torch.zeros(max(n, 1), dtype=torch.float64, device=self.dev)
+        res = None
+        for r in self.ranks:
+            rr = self._f2m.sweep_multi_result(self.ctl[r].data_ptr())
+            assert res is None or (rr["sweeps"], rr["converged"]) == (res["sweeps"], res["converged"])
+            res = rr
+            lo, hi = self.info[r]["begin"], self.info[r]["end"]
+            lam_pos[lo:hi] = self.rings[r][rr["out_buffer"]][lo:hi]
+        if not self.local:  # ranks own contiguous position ranges of different lengths: pad, gather
+            import torch.distributed as dist
+            width = max(1, -(-n // self.world) * 2)
+            lo, hi = self.info[self.comm.rank]["begin"], self.info[self.comm.rank]["end"]
+            mine = torch.zeros(width + 2, dtype=torch.float64, device=self.dev)
+            mine[0], mine[1] = float(lo), float(hi)
+            mine[2:2 + hi - lo] = lam_pos[lo:hi]
+            allv = torch.empty((self.world, width + 2), dtype=torch.float64, device=self.dev)
+            dist.all_gather_into_tensor(allv, mine)
+            for q in range(self.world):
+                a, z = int(allv[q, 0].item()), int(allv[q, 1].item())
+                lam_pos[a:z] = allv[q, 2:2 + z - a]
+        return lam_pos, res
+
+    def run(self, threshold: float, max_sweeps: int):
+        self.launch(threshold, max_sweeps)
+        torch.cuda.synchronize(self.dev)
+        lam_pos, res = self.collect()
+        ids = torch.empty(max(self.n, 1), dtype=torch.float64, device=self.dev)
+        if self.n > 0:
+            self._f2m.positions_to_ids(self.graph, lam_pos.data_ptr(), ids.data_ptr(),
+                                       torch.cuda.current_stream(self.dev).cuda_stream)
+        report = {"converged": res["converged"], "sweeps": res["sweeps"],
+                  "final_max_abs_delta": res["final_max_abs_delta"], "world": self.world, "g_total": self.g_total,
+                  "exchange": "resident"}
+        return ids[:self.n].cpu().numpy(), report
+
+
+def solve_duals_resident(inst, k: int, comm=None, eps: float = 1e-9, max_sweeps: int = 20000, **kw):
+    """solve_duals (dual.cpp:210-246) of build_knn_graph(inst, k) with the multi-GPU
+    partition-resident sweep kernel (ShardedResident). Returns (lambda, report) on every rank."""
+    if comm is None:
+        comm = TorchDistComm()
+    eng = ShardedResident(inst, k, comm, **kw)
+    threshold = eps * eng.graph.mean_cost()  # dual.cpp:221 (host fp64 product, no FMA)
+    return eng.run(threshold, max_sweeps)

@@ -378,3 +378,60 @@ def test_p2p_plan_arrays_degenerate_worlds():
     for sp, speer, sdst in ((sp1, speer1, sdst1), (sp2, speer2, sdst2)):
         for pos, r, d in zip(sp, speer, sdst):
             assert [rp1, rp2][r - 1][d] == pos
+
+
+# ------------------------------------------------------------------ multi-GPU partition-resident kernel
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_local_resident_ranks_match_single_gpu(world):
+    """world concurrent launches of the partition-resident sweep kernel on one GPU, each running
+    its share of a world x Gp partition and storing LL / max rings into every rank's copy."""
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_resident
+
+    inst = f2m.generate_instance(10000, 1, 1000.0)
+    g = f2m.build_knn_graph(inst, 10)
+    st, rep = f2m.solve_duals(g)
+    lam, srep = solve_duals_resident(inst, 10, LocalComm(world))
+    assert srep["sweeps"] == rep["sweeps"] == 3165 and srep["converged"]
+    assert srep["final_max_abs_delta"] == rep["final_max_abs_delta"]
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
+def test_local_resident_ranks_100k_and_truncated():
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, ShardedResident
+
+    inst = f2m.generate_instance(100000, 1, 1000.0)
+    g = f2m.build_knn_graph(inst, 10)
+    st, rep = f2m.solve_duals(g, max_sweeps=200000)
+    eng = ShardedResident(inst, 10, LocalComm(2))
+    lam, srep = eng.run(1e-9 * eng.graph.mean_cost(), 200000)
+    assert srep["sweeps"] == rep["sweeps"] == 6359
+    assert np.array_equal(lam, np.asarray(st.lam))
+    st2 = f2m.make_initial_state(g)
+    f2m.jacobi_sweeps(g, st2, 57)
+    lam2, srep2 = eng.run(-1.0, 57)
+    assert srep2["sweeps"] == 57 and not srep2["converged"]
+    assert np.array_equal(lam2, np.asarray(st2.lam))
+
+
+@pytest.mark.gpu
+def test_nccl_world1_resident_matches_single_gpu():
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import TorchDistComm, solve_duals_resident
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        inst = f2m.generate_instance(3000, 4, 1000.0)
+        st, rep = f2m.solve_duals(f2m.build_knn_graph(inst, 10))
+        lam, srep = solve_duals_resident(inst, 10, TorchDistComm())
+        assert srep["sweeps"] == rep["sweeps"]
+        assert np.array_equal(lam, np.asarray(st.lam))
+    finally:
+        dist.destroy_process_group()
