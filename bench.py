@@ -25,7 +25,8 @@ node-sharded engine on the 2M-city instance split across the N r
 exchange of the multipliers other ranks read, NCCL all-to-all per sweep), per-sweep device time
 over a fixed sweep count, and `sharded_2m_p2p`: the same sweeps through the fused peer-memory
 engine (one persistent kernel per rank; reported as unavailable if peer memory cannot be set up;
-with N > 1 only when F2M_BENCH_P2P=1).
+with N > 1 only when F2M_BENCH_P2P=1), and `sharded_2m_resident`: the same sweeps through the
+partition-resident kernel across ranks (same gating).
 """
 from __future__ import annotations
 
@@ -239,6 +240,32 @@ def sharded_leg(args, ws, rank, local, dev, n=2_000_000, sweeps=256, chunk=32):
                       "CUDA-graph replay"}, g, comm
 
 
+def sharded_resident_leg(comm, dev, n=2_000_000, sweeps=256):
+    """The 2M sweeps through the partition-resident kernel across ranks (sharded.ShardedResident:
+    the one-GPU persistent kernel with world x (SMs-1) partition CTAs, LL / max rings in every
+    rank's memory)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import ShardedResident
+
+    eng = ShardedResident(f2m.generate_instance(n, SEED, 1000.0), K, comm)
+    eng.run(-1.0, 8)  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.launch(-1.0, sweeps, e0, e1)
+    torch.cuda.synchronize()
+    _, res = eng.collect()
+    assert res["sweeps"] == sweeps
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    per_us = float(ms.item()) * 1e3 / sweeps
+    return {"workload": f"same as sharded_2m, partition-resident engine x{comm.world}",
+            "ranks": comm.world, "us_per_sweep": per_us, "gdp_iterations_per_s": 1e6 / per_us,
+            "algorithmic_GBps": eng.graph.sweep_bytes() / (per_us * 1e-6) / 1e9,
+            "partition_ctas": eng.g_total, "kernel": f2m.last_sweep_kernel_desc()}
+
+
 def sharded_p2p_leg(g, comm, dev, sweeps=256):
     """The same 2M sweeps through the fused peer-memory engine (one persistent kernel per rank,
     halo and sweep maxima stored into the peers' memory; sharded.ShardedP2P)."""
@@ -415,6 +442,10 @@ def run_gpu(args):
             line["sharded_2m_p2p"] = sharded_p2p_leg(sharded_ctx[0], sharded_ctx[1], dev)
         except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
             line["sharded_2m_p2p"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+        try:
+            line["sharded_2m_resident"] = sharded_resident_leg(sharded_ctx[1], dev)
+        except Exception as exc:  # noqa: BLE001
+            line["sharded_2m_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     import torch.distributed as dist

@@ -1897,6 +1897,9 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.npeers = world;
     a.ll_peers = d_ll_peers;
     a.cmax_peers = d_cmax_peers;
+    g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg->b) + (t.resident ? ", resident, 768" : ", streaming, 1024") +
+                        "> multi-rank (rank " + std::to_string(rank) + "/" + std::to_string(world) + ": " +
+                        std::to_string(Gp) + " of " + std::to_string(G) + " partition CTAs + 1 master, LL rings in every rank's memory)";
     if (t.resident) dispatch_sweep5<true, 768>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
     else dispatch_sweep5<false, 1024>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
     launched("gdp_sweep5_multi");

@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--local", type=int, default=0, help="simulate this many shards in one process")
     ap.add_argument("--solve", action="store_true")
-    ap.add_argument("--exchange", default="halo", choices=["halo", "allgather", "p2p"])
+    ap.add_argument("--exchange", default="halo", choices=["halo", "allgather", "p2p", "resident"])
     args = ap.parse_args()
 
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -42,8 +42,8 @@ def main():
     import torch.distributed as dist
 
     import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200.sharded import (LocalComm, ShardedJacobi, ShardedP2P, TorchDistComm,
-                                               make_halo_schedule, solve_duals_sharded)
+    from paper_2011_08170_b200.sharded import (LocalComm, ShardedJacobi, ShardedP2P, ShardedResident,
+                                               TorchDistComm, make_halo_schedule, solve_duals_sharded)
     from paper_2011_08170_b200 import _f2m
 
     f2m.set_device(local)
@@ -55,6 +55,28 @@ def main():
         dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=torch.device("cuda", local))
         comm = TorchDistComm()
     gen = f2m.generate_clustered_instance if args.clustered else f2m.generate_instance
+    if args.exchange == "resident":  # the partition-resident kernel across ranks (fixed sweep count)
+        dev = torch.device("cuda", local)
+        eng = ShardedResident(gen(args.n, args.seed), 10, comm)
+        eng.run(-1.0, max(args.warmup, 2))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.launch(-1.0, args.sweeps, e0, e1)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if not args.local:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        per = ms * 1e3 / args.sweeps
+        line = {"n": args.n, "m": eng.graph.m, "world": comm.world, "exchange": "resident", "sweeps": args.sweeps,
+                "us_per_sweep": per, "gdp_iterations_per_s": 1e6 / per, "g_total": eng.g_total,
+                "algorithmic_GBps": eng.graph.sweep_bytes() / (per * 1e-6) / 1e9,
+                "kernel": f2m.last_sweep_kernel_desc()}
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if not args.local:
+            dist.destroy_process_group()
+        return
     t0 = time.perf_counter()
     g = f2m.build_knn_graph(gen(args.n, args.seed), 10)
     t_graph = time.perf_counter() - t0
