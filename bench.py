@@ -26,7 +26,7 @@ exchange of the multipliers other ranks read, NCCL all-to-all per sweep), per-sw
 over a fixed sweep count, and `sharded_2m_p2p`: the same sweeps through the fused peer-memory
 engine (one persistent kernel per rank; reported as unavailable if peer memory cannot be set up;
 with N > 1 only when F2M_BENCH_P2P=1), and `sharded_2m_resident`: the same sweeps through the
-partition-resident kernel across ranks (same gating).
+partition-resident kernel across ranks.
 """
 from __future__ import annotations
 
@@ -437,15 +437,16 @@ def run_gpu(args):
     # last: an exchange failure here cannot disturb the legs above. Across processes the peer
     # buffers need a collective rendezvous (torch symmetric memory); a rank that failed before it
     # would leave the others waiting, so N > 1 runs it only on request (F2M_BENCH_P2P=1)
+    if sharded_ctx is not None:
+        try:  # the partition-resident engine: every rank builds, allocates and rendezvouses alike
+            line["sharded_2m_resident"] = sharded_resident_leg(sharded_ctx[1], dev)
+        except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
+            line["sharded_2m_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     if sharded_ctx is not None and (ws == 1 or os.environ.get("F2M_BENCH_P2P") == "1"):
         try:
             line["sharded_2m_p2p"] = sharded_p2p_leg(sharded_ctx[0], sharded_ctx[1], dev)
-        except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
-            line["sharded_2m_p2p"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
-        try:
-            line["sharded_2m_resident"] = sharded_resident_leg(sharded_ctx[1], dev)
         except Exception as exc:  # noqa: BLE001
-            line["sharded_2m_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+            line["sharded_2m_p2p"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     import torch.distributed as dist
