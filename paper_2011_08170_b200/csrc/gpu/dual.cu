@@ -415,6 +415,7 @@ struct Sweep4Args {
   int npeers;
   unsigned long long* const* ll_peers;
   unsigned long long* const* cmax_peers;
+  const uint32_t* __restrict__ ll_mask;  // [nb] ranks that read each boundary node
 };
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
@@ -624,13 +625,15 @@ __device__ __forceinline__ void st_ll_sys(unsigned long long* p, double v, unsig
 
 // LL stores of the sweep kernel; in the multi-GPU form into every rank's ring (same offset,
 // system scope: the readers are on other GPUs)
-__device__ __forceinline__ void publish_ll(const Sweep4Args& a, unsigned long long* local, double v, unsigned tag) {
+__device__ __forceinline__ void publish_ll(const Sweep4Args& a, unsigned long long* ring, int idx, double v,
+                                           unsigned tag) {
   if (!a.npeers) {
-    st_ll(local, v, tag);
+    st_ll(ring + 2 * idx, v, tag);
     return;
   }
-  const size_t off = (size_t)(local - a.ll);
-  for (int q = 0; q < a.npeers; ++q) st_ll_sys(a.ll_peers[q] + off, v, tag);
+  // only the ranks whose CTAs read this boundary node (bit q of ll_mask[idx])
+  const size_t off = (size_t)(ring - a.ll) + 2 * (size_t)idx;
+  for (unsigned m = a.ll_mask[idx]; m; m &= m - 1) st_ll_sys(a.ll_peers[__ffs(m) - 1] + off, v, tag);
 }
 __device__ __forceinline__ void publish_cmax(const Sweep4Args& a, size_t off, double v, unsigned tag) {
   if (!a.npeers) {
@@ -901,7 +904,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         if (node < nbnd && half == 0) {
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (lp >= nint) publish_ll(a, llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
           gout[p] = nl;
           lam_next[lp] = nl;
           const double ad = fabs(d);
@@ -955,7 +958,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           }
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (lp >= nint) publish_ll(a, llout + 2 * (bo + lp), nl, (unsigned)s + 1);
+          if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
           gout[p] = nl;
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
@@ -1288,6 +1291,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.npeers = 0;
     a.ll_peers = nullptr;
     a.cmax_peers = nullptr;
+    a.ll_mask = nullptr;
     a.trace_first = a.trace_count = 0;
     DBuf<unsigned long long> trace;
     if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {
@@ -1840,6 +1844,17 @@ extern "C" int f2m_sweep_multi_info(const f2m_graph* g, int rank, int world, int
 
 extern "C" size_t f2m_sweep_multi_ctl_bytes(void) { return sizeof(f2mgpu::Sweep4Ctl); }
 
+namespace f2mgpu {
+// bit r of mask[i]: a CTA of rank r has LL entry i (a boundary node of another CTA) in its halo
+__global__ void k_ll_mask(int G, int gp, const int32_t* __restrict__ halo_off, const int32_t* __restrict__ halo_pub,
+                          uint32_t* __restrict__ mask) {
+  const int c = blockIdx.x;
+  if (c >= G) return;
+  const uint32_t bit = 1u << (c / gp);
+  for (int h = halo_off[c] + threadIdx.x; h < halo_off[c + 1]; h += blockDim.x) atomicOr(&mask[halo_pub[h]], bit);
+}
+}  // namespace f2mgpu
+
 extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_config* cfg, int rank, int world,
                                       double* d_ring, unsigned long long* d_ll,
                                       unsigned long long* const* d_ll_peers, unsigned long long* d_cmax,
@@ -1897,6 +1912,14 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.npeers = world;
     a.ll_peers = d_ll_peers;
     a.cmax_peers = d_cmax_peers;
+    if (world > 32) throw Error(F2M_E_ARGUMENT, "multi sweep: at most 32 ranks");
+    DBuf<uint32_t> mask((size_t)a.nb, s);
+    F2M_CUDA(cudaMemsetAsync(mask.get(), 0, mask.bytes(), s));
+    if (G > 0) {
+      k_ll_mask<<<G, 128, 0, s>>>(G, Gp, t.halo_off.get(), t.halo_pub.get(), mask.get());
+      launched("ll_mask");
+    }
+    a.ll_mask = mask.get();  // freed (stream-ordered) after the sweep kernel
     g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg->b) + (t.resident ? ", resident, 768" : ", streaming, 1024") +
                         "> multi-rank (rank " + std::to_string(rank) + "/" + std::to_string(world) + ": " +
                         std::to_string(Gp) + " of " + std::to_string(G) + " partition CTAs + 1 master, LL rings in every rank's memory)";
