@@ -605,6 +605,8 @@ class ShardedResident:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         # one SM per rank's master; in-process ranks share this device's SMs
         gp = ctas_per_rank or (max(1, (sms - world) // world) if local else sms - 1)
+        nslices = -(-int(inst.points_array().shape[0]) // 32)
+        gp = max(1, min(gp, nslices // world))  # every partition CTA needs at least one 32-row slice
         _f2m.set_sweep_partition(world * gp)
         try:
             self.graph = f2m.build_knn_graph(inst, k)

@@ -399,6 +399,19 @@ def test_local_resident_ranks_match_single_gpu(world):
 
 
 @pytest.mark.gpu
+def test_local_resident_ranks_small_graph():
+    """A graph with fewer 32-row slices than SMs: the per-rank partition shrinks to fit."""
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, solve_duals_resident
+
+    inst = f2m.generate_instance(1000, 3, 1000.0)
+    st, rep = f2m.solve_duals(f2m.build_knn_graph(inst, 10))
+    lam, srep = solve_duals_resident(inst, 10, LocalComm(4))
+    assert srep["sweeps"] == rep["sweeps"] and srep["g_total"] <= 32
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
 def test_local_resident_ranks_100k_and_truncated():
     import paper_2011_08170_b200 as f2m
     from paper_2011_08170_b200.sharded import LocalComm, ShardedResident
