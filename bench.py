@@ -26,7 +26,8 @@ exchange of the multipliers other ranks read, NCCL all-to-all per sweep), per-sw
 over a fixed sweep count, and `sharded_2m_p2p`: the same sweeps through the fused peer-memory
 engine (one persistent kernel per rank; reported as unavailable if peer memory cannot be set up;
 with N > 1 only when F2M_BENCH_P2P=1), and `sharded_2m_resident`: the same sweeps through the
-partition-resident kernel across ranks.
+partition-resident kernel across ranks, and `clustered_200k_resident`: BASELINE configs[3]
+(clustered 200k) solved to convergence by that engine across the N ranks.
 """
 from __future__ import annotations
 
@@ -266,6 +267,30 @@ def sharded_resident_leg(comm, dev, n=2_000_000, sweeps=256):
             "partition_ctas": eng.g_total, "kernel": f2m.last_sweep_kernel_desc()}
 
 
+def clustered_resident_leg(comm, dev, n=200_000):
+    """BASELINE configs[3]: clustered 200k cities, solve_duals to convergence (eps 1e-9) with the
+    partition-resident engine across the N ranks; device time of the solve (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import ShardedResident
+
+    eng = ShardedResident(f2m.generate_clustered_instance(n, SEED), K, comm)
+    thr = EPS * eng.graph.mean_cost()
+    eng.run(thr, MAX_SWEEPS)  # warm-up (same solve)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.launch(thr, MAX_SWEEPS, e0, e1)
+    torch.cuda.synchronize()
+    _, res = eng.collect()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return {"workload": f"clustered {n} cities (seed {SEED}), k={K}, solve_duals to eps {EPS:g} "
+                        f"(BASELINE configs[3]), partition-resident engine x{comm.world}",
+            "ranks": comm.world, "solve_duals_ms": float(ms.item()), "sweeps": res["sweeps"],
+            "converged": res["converged"], "us_per_sweep": 1e3 * float(ms.item()) / max(res["sweeps"], 1)}
+
+
 def sharded_p2p_leg(g, comm, dev, sweeps=256):
     """The same 2M sweeps through the fused peer-memory engine (one persistent kernel per rank,
     halo and sweep maxima stored into the peers' memory; sharded.ShardedP2P)."""
@@ -442,6 +467,11 @@ def run_gpu(args):
             line["sharded_2m_resident"] = sharded_resident_leg(sharded_ctx[1], dev)
         except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
             line["sharded_2m_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+    if sharded_ctx is not None:
+        try:
+            line["clustered_200k_resident"] = clustered_resident_leg(sharded_ctx[1], dev)
+        except Exception as exc:  # noqa: BLE001
+            line["clustered_200k_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     if sharded_ctx is not None and (ws == 1 or os.environ.get("F2M_BENCH_P2P") == "1"):
         try:
             line["sharded_2m_p2p"] = sharded_p2p_leg(sharded_ctx[0], sharded_ctx[1], dev)
