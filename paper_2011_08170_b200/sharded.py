@@ -679,7 +679,10 @@ class ShardedResident:
             lam_pos[lo:hi] = self.rings[r][rr["out_buffer"]][lo:hi]
         if not self.local:  # ranks own contiguous position ranges of different lengths: pad, gather
             import torch.distributed as dist
-            width = max(1, -(-n // self.world) * 2)
+            if not hasattr(self, "_width"):  # the longest rank range (identical topology on every rank)
+                spans = [self._f2m.sweep_multi_info(self.graph, q, self.world) for q in range(self.world)]
+                self._width = max(1, max(x["end"] - x["begin"] for x in spans))
+            width = self._width
             lo, hi = self.info[self.comm.rank]["begin"], self.info[self.comm.rank]["end"]
             mine = torch.zeros(width + 2, dtype=torch.float64, device=self.dev)
             mine[0], mine[1] = float(lo), float(hi)
