@@ -1829,6 +1829,7 @@ extern "C" int f2m_sweep_multi_info(const f2m_graph* g, int rank, int world, int
     const Topology& t = *g->topo;
     if (!t.v2) throw Error(F2M_E_ARGUMENT, "multi sweep: the graph has no partition-resident layout");
     if (world < 1 || t.sweep_ctas % world) throw Error(F2M_E_ARGUMENT, "multi sweep: partition not divisible by world");
+    if (rank < 0 || rank >= world) throw Error(F2M_E_INDEX, "multi sweep: rank outside [0, world)");
     const int G = t.sweep_ctas, Gp = G / world;
     *g_total = G;
     *resident = t.resident ? 1 : 0;
@@ -1864,7 +1865,8 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     using namespace f2mgpu;
     validate_engine(*cfg);
     const Topology& t = *g->topo;
-    if (!t.v2 || t.sweep_ctas % world) throw Error(F2M_E_ARGUMENT, "multi sweep: bad partition");
+    if (world < 1 || !t.v2 || t.sweep_ctas % world) throw Error(F2M_E_ARGUMENT, "multi sweep: bad partition");
+    if (rank < 0 || rank >= world) throw Error(F2M_E_INDEX, "multi sweep: rank outside [0, world)");
     if (t.n > 0 && t.min_deg <= cfg->b)
       throw Error(F2M_E_DEGREE, "node has degree " + std::to_string(t.min_deg) + " <= b = " + std::to_string(cfg->b));
     const int G = t.sweep_ctas, Gp = G / world;

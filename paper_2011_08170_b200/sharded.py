@@ -60,7 +60,14 @@ class TorchDistComm:
 
 class LocalComm:
     """All shards in this process (simulated ranks on one device): the all-gather is the ordered
-    concatenation, the all-reduce an element-wise max. Same schedule as TorchDistComm."""
+    concatenation, the all-reduce an element-wise max. Same schedule as TorchDistComm.
+
+    Test-only for the persistent engines (ShardedP2P, ShardedResident): their in-process ranks are
+    `world` cooperative launches on separate streams of ONE device that spin-wait on each other,
+    and CUDA guarantees co-residency only inside one grid, not across grids. They run concurrently
+    on an otherwise idle device (the SMs are split between them) and every poll has a 20 s watchdog
+    that aborts instead of hanging; production multi-GPU runs one rank per device (TorchDistComm
+    across processes, or DeviceComm in one process)."""
 
     def __init__(self, world: int):
         self.rank = 0
@@ -512,7 +519,7 @@ class ShardedP2P:
         torch.cuda.synchronize(self.dev)  # buffers zeroed before any rank publishes
         if not self.local:
             import torch.distributed as dist
-            dist.barrier()
+            dist.barrier(group=self.comm.group)
         cur = torch.cuda.current_stream(self.dev)
         if ev_start is not None:
             ev_start.record(cur)
@@ -580,6 +587,20 @@ def _solve_duals_p2p(graph, comm, eps, max_sweeps, b, eta, update, init, thresho
     return ids[:n].cpu().numpy(), report
 
 
+def gather_ranges(comm, vec: torch.Tensor, lo: int, hi: int, width: int) -> None:
+    """Every rank owns the contiguous range vec[lo:hi] (ranges of different lengths, at most
+    `width`); afterwards every rank's `vec` holds all ranks' ranges. One padded all-gather over
+    comm's group: each rank contributes [lo, hi, values..., padding]."""
+    mine = torch.zeros(width + 2, dtype=vec.dtype, device=vec.device)
+    mine[0], mine[1] = float(lo), float(hi)
+    mine[2:2 + hi - lo] = vec[lo:hi]
+    allv = torch.empty((comm.world, width + 2), dtype=vec.dtype, device=vec.device)
+    comm.all_gather(allv.view(-1), [mine])
+    for q in range(comm.world):
+        a, z = int(allv[q, 0].item()), int(allv[q, 1].item())
+        vec[a:z] = allv[q, 2:2 + z - a]
+
+
 class ShardedResident:
     """The one-GPU partition-resident sweep kernel (k_gdp_sweep5) spread over ranks: the graph is
     built once per rank with world x Gp partition CTAs (f2m_set_sweep_partition), rank r runs CTAs
@@ -597,6 +618,10 @@ class ShardedResident:
 
         self._f2m = _f2m
         self.comm = comm
+        nslices = -(-int(inst.points_array().shape[0]) // 32)
+        if nslices < comm.world:
+            raise ValueError(f"ShardedResident: {nslices} 32-row slices cannot be split over {comm.world} ranks "
+                             f"(every rank needs at least one partition CTA); use fewer ranks")
         self.b, self.eta, self.update = b, eta, update
         self.dev = dev = torch.device("cuda", torch.cuda.current_device())
         self.world = world = comm.world
@@ -605,7 +630,6 @@ class ShardedResident:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         # one SM per rank's master; in-process ranks share this device's SMs
         gp = ctas_per_rank or (max(1, (sms - world) // world) if local else sms - 1)
-        nslices = -(-int(inst.points_array().shape[0]) // 32)
         gp = max(1, min(gp, nslices // world))  # every partition CTA needs at least one 32-row slice
         _f2m.set_sweep_partition(world * gp)
         try:
@@ -651,7 +675,7 @@ class ShardedResident:
         torch.cuda.synchronize(self.dev)  # rings zeroed on every rank before any rank publishes
         if not self.local:
             import torch.distributed as dist
-            dist.barrier()
+            dist.barrier(group=self.comm.group)
         cur = torch.cuda.current_stream(self.dev)
         if ev_start is not None:
             ev_start.record(cur)
@@ -678,20 +702,11 @@ class ShardedResident:
             lo, hi = self.info[r]["begin"], self.info[r]["end"]
             lam_pos[lo:hi] = self.rings[r][rr["out_buffer"]][lo:hi]
         if not self.local:  # ranks own contiguous position ranges of different lengths: pad, gather
-            import torch.distributed as dist
             if not hasattr(self, "_width"):  # the longest rank range (identical topology on every rank)
                 spans = [self._f2m.sweep_multi_info(self.graph, q, self.world) for q in range(self.world)]
                 self._width = max(1, max(x["end"] - x["begin"] for x in spans))
-            width = self._width
             lo, hi = self.info[self.comm.rank]["begin"], self.info[self.comm.rank]["end"]
-            mine = torch.zeros(width + 2, dtype=torch.float64, device=self.dev)
-            mine[0], mine[1] = float(lo), float(hi)
-            mine[2:2 + hi - lo] = lam_pos[lo:hi]
-            allv = torch.empty((self.world, width + 2), dtype=torch.float64, device=self.dev)
-            dist.all_gather_into_tensor(allv, mine)
-            for q in range(self.world):
-                a, z = int(allv[q, 0].item()), int(allv[q, 1].item())
-                lam_pos[a:z] = allv[q, 2:2 + z - a]
+            gather_ranges(self.comm, lam_pos, lo, hi, self._width)
         return lam_pos, res
 
     def run(self, threshold: float, max_sweeps: int):

@@ -448,3 +448,40 @@ def test_nccl_world1_resident_matches_single_gpu():
         assert np.array_equal(lam, np.asarray(st.lam))
     finally:
         dist.destroy_process_group()
+
+
+def _gather_ranges_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    from paper_2011_08170_b200.sharded import TorchDistComm, gather_ranges
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # a subgroup of ranks {1, 2}: the gather must run over the subgroup only (rank 0 never joins)
+        sub = dist.new_group([1, 2])
+        if rank in (1, 2):
+            comm = TorchDistComm(group=sub)
+            n = 11
+            spans = [(0, 7), (7, 11)]  # ragged ranges, width 7
+            lo, hi = spans[comm.rank]
+            vec = torch.full((n,), -1.0, dtype=torch.float64)
+            vec[lo:hi] = torch.arange(lo, hi, dtype=torch.float64) * 10 + comm.rank
+            gather_ranges(comm, vec, lo, hi, 7)
+            np.save(f"{out_path}.{rank}.npy", vec.numpy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_gather_ranges_subgroup(tmp_path):
+    """ShardedResident.collect's padded gather of ragged rank ranges, over a process subgroup
+    (world 3, group {1, 2}): every member ends with all ranges."""
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "g")
+    mp.spawn(_gather_ranges_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    want = np.array([i * 10 + (0 if i < 7 else 1) for i in range(11)], np.float64)
+    for r in (1, 2):
+        assert np.array_equal(np.load(f"{out}.{r}.npy"), want)
