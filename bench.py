@@ -179,6 +179,27 @@ def _dist():
     return ws, rank, local
 
 
+def _agree(ok: bool) -> bool:
+    """True iff every rank is ok (MIN all-reduce; always the local flag without a process group).
+    Called before each multi-rank leg's collective section so that a rank that failed in its
+    rank-local setup makes ALL ranks skip the collectives instead of leaving the others blocked."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return ok
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+def _summary():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def _cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -286,54 +307,217 @@ def sharded_leg(args, ws, rank, local, dev, n=2_000_000, sweeps=256, chunk=32):
                       "CUDA-graph replay"}, g, comm
 
 
+def _resident_engine(inst, comm):
+    """ShardedResident for a multi-rank leg: rank-local setup, then agreement across ranks before
+    the collective rendezvous (connect). Returns (engine or None, error or None)."""
+    from paper_2011_08170_b200.sharded import ShardedResident
+    eng, err = None, None
+    try:
+        eng = ShardedResident(inst, K, comm)
+    except Exception as exc:  # noqa: BLE001 - reported in the line
+        err = f"{type(exc).__name__}: {exc}"[:200]
+    if not _agree(err is None):
+        return None, err or "another rank failed its setup"
+    eng.connect()
+    return eng, None
+
+
+def _timed_resident(eng, threshold, max_sweeps, dev):
+    """One launch of the engine to `threshold` (or max_sweeps), device time max over ranks."""
+    import torch
+    import torch.distributed as dist
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.launch(threshold, max_sweeps, e0, e1)
+    torch.cuda.synchronize()
+    ok, res, lam_pos = True, None, None
+    try:
+        lam_pos, res = eng.collect_local()
+    except Exception:  # noqa: BLE001 - a watchdog abort on this rank
+        ok = False
+    if not _agree(ok):
+        raise RuntimeError("resident engine: a rank's sweep kernel aborted")
+    lam_pos = eng.gather(lam_pos)
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if dist.is_initialized():
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return float(ms.item()), res, lam_pos
+
+
 def sharded_resident_leg(comm, dev, n=2_000_000, sweeps=256):
     """The 2M sweeps through the partition-resident kernel across ranks (sharded.ShardedResident:
     the one-GPU persistent kernel with world x (SMs-1) partition CTAs, LL / max rings in every
     rank's memory)."""
-    import torch
-    import torch.distributed as dist
-
     import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200.sharded import ShardedResident
 
-    eng = ShardedResident(f2m.generate_instance(n, SEED, 1000.0), K, comm)
-    eng.run(-1.0, 8)  # warm-up
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eng.launch(-1.0, sweeps, e0, e1)
-    torch.cuda.synchronize()
-    _, res = eng.collect()
+    eng, err = _resident_engine(f2m.generate_instance(n, SEED, 1000.0), comm)
+    if eng is None:
+        return {"unavailable": err}
+    _timed_resident(eng, -1.0, 8, dev)  # warm-up
+    ms, res, _ = _timed_resident(eng, -1.0, sweeps, dev)
     assert res["sweeps"] == sweeps
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    per_us = float(ms.item()) * 1e3 / sweeps
+    per_us = ms * 1e3 / sweeps
     return {"workload": f"same as sharded_2m, partition-resident engine x{comm.world}",
             "ranks": comm.world, "us_per_sweep": per_us, "gdp_iterations_per_s": 1e6 / per_us,
             "algorithmic_GBps": eng.graph.sweep_bytes() / (per_us * 1e-6) / 1e9,
-            "partition_ctas": eng.g_total, "kernel": f2m.last_sweep_kernel_desc()}
+            "partition_ctas": eng.g_total, "smem_resident": eng.resident,
+            "nvlink_bytes_per_sweep_per_rank": eng.peer_bytes_per_sweep(),
+            "kernel": f2m.last_sweep_kernel_desc()}
+
+
+def _certify(graph, lam_ids, eps=EPS):
+    """extract_primal + verify_solution (primal.cpp:142-276) on converged multipliers, one attempt
+    (no restarts): objective, gap, feasibility — or the reference's own extraction failure."""
+    import paper_2011_08170_b200 as f2m
+    st = f2m.DualState(list(lam_ids))
+    tol = max(1e-7, 10 * eps) * graph.mean_cost()  # solve.cpp:16-18, :64
+    try:
+        sol = f2m.extract_primal(graph, st, tol)
+        rep = f2m.verify_solution(graph, sol, st)
+        return {"objective": sol.objective, "gap": rep["duality_gap"], "feasible": bool(rep["feasible"]),
+                "certified": bool(rep["feasible"]) and rep["duality_gap"] <= 1e-6 * (1 + abs(sol.objective))}
+    except Exception as exc:  # noqa: BLE001
+        return {"extraction": f"{type(exc).__name__}: {exc}"[:200], "certified": False}
 
 
 def clustered_resident_leg(comm, dev, n=200_000):
-    """BASELINE configs[3]: clustered 200k cities, solve_duals to convergence (eps 1e-9) with the
-    partition-resident engine across the N ranks; device time of the solve (max over ranks)."""
+    """BASELINE configs[3]: clustered 200k cities solved to convergence (eps 1e-9) with the
+    partition-resident engine across the N ranks, then extraction + certificate on rank 0."""
+    import paper_2011_08170_b200 as f2m
+
+    eng, err = _resident_engine(f2m.generate_clustered_instance(n, SEED), comm)
+    if eng is None:
+        return {"unavailable": err}
+    thr = EPS * eng.graph.mean_cost()
+    _timed_resident(eng, thr, MAX_SWEEPS, dev)  # warm-up (same solve)
+    ms, res, lam_pos = _timed_resident(eng, thr, MAX_SWEEPS, dev)
+    out = {"workload": f"clustered {n} cities (seed {SEED}), k={K}, solve_duals to eps {EPS:g} "
+                       f"(BASELINE configs[3]), partition-resident engine x{comm.world}",
+           "ranks": comm.world, "solve_duals_ms": ms, "sweeps": res["sweeps"],
+           "converged": res["converged"], "us_per_sweep": 1e3 * ms / max(res["sweeps"], 1)}
+    if comm.rank == 0:
+        out["certificate"] = _certify(eng.graph, eng.to_ids(lam_pos))
+    return out
+
+
+def certified_solve_leg(name, points, dev, steps=3, warmup=2, golden=None):
+    """A certified full solve (the headline pipeline, f2m_full_solve_device) of another BASELINE
+    configuration on one GPU: device time per solve, sweeps, objective/gap and, when a reference
+    golden exists, whether the result equals the reference's own run bit for bit."""
     import torch
-    import torch.distributed as dist
 
     import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200.sharded import ShardedResident
+    n = points.shape[0]
+    d_xy = torch.from_numpy(points).to(dev)
+    d_x = torch.empty(n * K, dtype=torch.float64, device=dev)
+    d_lam = torch.empty(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    eng = ShardedResident(f2m.generate_clustered_instance(n, SEED), K, comm)
-    thr = EPS * eng.graph.mean_cost()
-    eng.run(thr, MAX_SWEEPS)  # warm-up (same solve)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eng.launch(thr, MAX_SWEEPS, e0, e1)
-    torch.cuda.synchronize()
-    _, res = eng.collect()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    return {"workload": f"clustered {n} cities (seed {SEED}), k={K}, solve_duals to eps {EPS:g} "
-                        f"(BASELINE configs[3]), partition-resident engine x{comm.world}",
-            "ranks": comm.world, "solve_duals_ms": float(ms.item()), "sweeps": res["sweeps"],
-            "converged": res["converged"], "us_per_sweep": 1e3 * float(ms.item()) / max(res["sweeps"], 1)}
+    def solve():
+        return f2m.full_solve_device(n, d_xy.data_ptr(), False, K, EPS, MAX_SWEEPS, d_x.data_ptr(), n * K,
+                                     d_lam.data_ptr())
+    for _ in range(warmup):
+        solve()
+    times, kern = [], []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        r = solve()
+        times.append(r["t_total"])
+        kern.append(f2m.last_sweep_kernel())
+    ms, sw = kern[-1]
+    out = {"workload": name, "n": n, "steps": steps, "time_to_solve_s": statistics.mean(times),
+           "sweeps": r["sweeps"], "restarts": r["restarts"], "objective": r["objective"], "gap": r["gap"],
+           "feasible": bool(r["feasible"]), "gdp_iterations_per_s": sw / (ms * 1e-3),
+           "us_per_sweep": 1e3 * ms / max(sw, 1), "sweep_kernel": f2m.last_sweep_kernel_desc(),
+           "stage_s": {"knn": r["t_knn"], "duals": r["t_duals"], "extract_verify": r["t_extract"]}}
+    if golden is not None:
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", golden + ".json")) as f:
+                g = json.load(f)
+            out["equals_reference_run"] = (r["objective"] == g["full_objective"] and r["gap"] == g["full_gap"]
+                                           and r["sweeps"] == g["full_sweeps"])
+            out["reference_cpu_s_1_thread"] = g.get("t_full")
+        except Exception:  # noqa: BLE001
+            pass
+    return out
+
+
+def uniform_2m_leg(comm, dev, n=2_000_000):
+    """BASELINE configs[4]: the 2M uniform instance solved to convergence (eps 1e-9) across the N
+    ranks (partition-resident engine; at N = 1 the one-GPU solve_duals, streaming form), then one
+    extraction + certificate attempt on rank 0 (the reference's primal.cpp:142-276; its
+    exhaustive-search cap of 20 edges per zero component applies unchanged)."""
+    import time as _t
+
+    import numpy as np
+    import torch
+
+    import paper_2011_08170_b200 as f2m
+    inst = f2m.generate_instance(n, SEED, 1000.0)
+    out = {"workload": f"random-uniform {n} cities (seed {SEED}), k={K}, solve_duals to eps {EPS:g} "
+                       f"(BASELINE configs[4]) on {comm.world} GPU(s)", "ranks": comm.world}
+    if comm.world == 1:
+        t0 = _t.perf_counter()
+        g = f2m.build_knn_graph(inst, K)
+        torch.cuda.synchronize()
+        out["build_s"] = _t.perf_counter() - t0
+        f2m.solve_duals(g, eps=EPS, max_sweeps=MAX_SWEEPS)  # warm-up (allocations, mean)
+        st, rep = f2m.solve_duals(g, eps=EPS, max_sweeps=MAX_SWEEPS)
+        ms, sw = f2m.last_sweep_kernel()
+        out.update({"solve_duals_ms": ms, "sweeps": rep["sweeps"], "converged": rep["converged"],
+                    "dual_value": rep["dual_value"], "us_per_sweep": 1e3 * ms / max(sw, 1),
+                    "gdp_iterations_per_s": sw / (ms * 1e-3), "kernel": f2m.last_sweep_kernel_desc(),
+                    "reference_cpu_s_per_sweep_1_thread": 1.631})
+        lam_ids = np.asarray(st.lam)
+        graph = g
+    else:
+        eng, err = _resident_engine(inst, comm)
+        if eng is None:
+            return {**out, "unavailable": err}
+        thr = EPS * eng.graph.mean_cost()
+        _timed_resident(eng, -1.0, 8, dev)  # warm-up
+        ms, res, lam_pos = _timed_resident(eng, thr, MAX_SWEEPS, dev)
+        out.update({"solve_duals_ms": ms, "sweeps": res["sweeps"], "converged": res["converged"],
+                    "us_per_sweep": 1e3 * ms / max(res["sweeps"], 1),
+                    "gdp_iterations_per_s": res["sweeps"] / (ms * 1e-3), "partition_ctas": eng.g_total,
+                    "smem_resident": eng.resident, "nvlink_bytes_per_sweep_per_rank": eng.peer_bytes_per_sweep(),
+                    "kernel": f2m.last_sweep_kernel_desc()})
+        lam_ids = eng.to_ids(lam_pos) if comm.rank == 0 else None
+        graph = eng.graph
+    if comm.rank == 0:
+        out["certificate"] = _certify(graph, lam_ids)
+    return out
+
+
+def allpairs_leg(dev, sizes=((2000, 200), (8000, 30))):
+    """north_star's all-pairs scans: complete graphs (build_knn_graph with k >= n-1, graph.cpp:175)
+    whose sweeps recompute every distance from the points (k_allpairs_sweep). Fixed sweep counts;
+    the roofline is the FP64 pipe: fp64 instructions per launch (ncu, profiles/ncu_summary.json
+    allpairs_*) over the kernel time against the measured fp64 issue peak (tools/microbench/tput.cu)."""
+    import paper_2011_08170_b200 as f2m
+    summ = _summary()
+    peak = summ.get("fp64_peak", {})
+    out = []
+    for n, sweeps in sizes:
+        g = f2m.build_knn_graph(f2m.generate_instance(n, SEED, 1000.0), n - 1)
+        st = f2m.make_initial_state(g)
+        f2m.jacobi_sweeps(g, st, 5)  # warm-up
+        st = f2m.make_initial_state(g)
+        f2m.jacobi_sweeps(g, st, sweeps)
+        ms, sw = f2m.last_sweep_kernel()
+        assert "allpairs" in f2m.last_sweep_kernel_desc()
+        pairs = n * (n - 1) * sw
+        row = {"n": n, "sweeps": sw, "kernel_ms": ms, "us_per_sweep": 1e3 * ms / sw,
+               "pair_evaluations_per_s": pairs / (ms * 1e-3), "kernel": f2m.last_sweep_kernel_desc()}
+        prof = summ.get(f"allpairs_{n}")
+        if prof and peak.get("fp64_inst_per_s"):
+            achieved = prof["fp64_thread_inst_per_pair"] * pairs / (ms * 1e-3)
+            row["roofline"] = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak["fp64_inst_per_s"] / 1e12,
+                               "unit": "T fp64 thread-instructions/s", "frac": achieved / peak["fp64_inst_per_s"],
+                               "fp64_pipe_active_ncu": prof.get("fp64_pipe_active_pct"),
+                               "source": prof.get("source"), "peak_source": peak.get("source")}
+        out.append(row)
+    return out
 
 
 def sharded_p2p_leg(g, comm, dev, sweeps=256):
@@ -485,6 +669,18 @@ def run_gpu(args):
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
     }
+    # ---- the other BASELINE configurations, one GPU each (rank 0): certified full solves of the
+    # 200k uniform instance the metric names and of clustered 200k (configs[3]), and the all-pairs
+    # scans (north_star: FP64-pipe roofline)
+    if rank == 0 and not args.no_extra:
+        inst200 = f2m.generate_instance(200_000, SEED, 1000.0)
+        line["uniform_200k"] = certified_solve_leg(
+            "random-uniform 200,000 cities (seed 1), k=10, certified full solve", inst200.points_array(), dev,
+            golden="u200k_s1")
+        line["clustered_200k"] = certified_solve_leg(
+            "clustered 200,000 cities (seed 1), k=10, certified full solve (BASELINE configs[3], 1 GPU)",
+            f2m.generate_clustered_instance(200_000, SEED).points_array(), dev, golden="clust200k_s1")
+        line["allpairs"] = allpairs_leg(dev)
     # ---- node-sharded engine: the 2M-city instance (BASELINE configs[4]) split
     # across the N ranks, lambda all-gathered with NCCL every sweep; fixed sweep count (the full
     # 2M solve takes tens of thousands of sweeps), device time, max over ranks.
@@ -500,21 +696,20 @@ def run_gpu(args):
             "value": v, "unit": "s", "cores": 1, "kind": "reference", "cpu_model": _cpu_model(),
             "sample": (f"unmodified reference (oracle/_ref): build_knn_graph + init + {REF_SAMPLE_SWEEPS} Jacobi "
                        f"sweeps + extract/verify on the converged lambda, 1 thread; projected to "
-                       f"{sweeps_total} sweeps"),
+                       f"{sweeps_total} sweeps (the --impl reference arm times a complete stock full_solve)"),
             "detail": detail}
-    # last: an exchange failure here cannot disturb the legs above. Across processes the peer
-    # buffers need a collective rendezvous (torch symmetric memory); a rank that failed before it
-    # would leave the others waiting, so N > 1 runs it only on request (F2M_BENCH_P2P=1)
+    # multi-rank legs: each agrees across ranks (all-reduce of an ok flag) before its collectives,
+    # so a rank that fails its local setup makes every rank skip together instead of hanging
     if sharded_ctx is not None:
-        try:  # the partition-resident engine: every rank builds, allocates and rendezvouses alike
-            line["sharded_2m_resident"] = sharded_resident_leg(sharded_ctx[1], dev)
-        except Exception as exc:  # noqa: BLE001 - reported in the line, the NCCL leg stands
-            line["sharded_2m_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
-    if sharded_ctx is not None:
-        try:
-            line["clustered_200k_resident"] = clustered_resident_leg(sharded_ctx[1], dev)
-        except Exception as exc:  # noqa: BLE001
-            line["clustered_200k_resident"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+        comm2m = sharded_ctx[1]
+        for key, fn in (("uniform_2m", uniform_2m_leg), ("sharded_2m_resident", sharded_resident_leg),
+                        ("clustered_200k_resident", clustered_resident_leg)):
+            try:
+                line[key] = fn(comm2m, dev)
+            except Exception as exc:  # noqa: BLE001 - after an agreed failure every rank lands here
+                line[key] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+    # last: across processes the fused p2p engine needs a rendezvous with no agreement step, so
+    # N > 1 runs it only on request (F2M_BENCH_P2P=1)
     if sharded_ctx is not None and (ws == 1 or os.environ.get("F2M_BENCH_P2P") == "1"):
         try:
             line["sharded_2m_p2p"] = sharded_p2p_leg(sharded_ctx[0], sharded_ctx[1], dev)
@@ -535,7 +730,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-sharded", action="store_true", help="skip the node-sharded 2M leg")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the node-sharded 2M legs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the 200k / all-pairs legs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

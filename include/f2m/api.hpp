@@ -145,6 +145,9 @@ struct EngineConfig {
   UpdateRule update = UpdateRule::kMidpoint;
   DualInit init = DualInit::kLocalMidpoint;
   int threads = 0;  // accepted for compatibility; the device picks its own grid
+  // B200 extension (f2m_engine_config.num_gpus): > 1 runs solve_duals' Jacobi sweeps on that many
+  // GPUs from the calling thread (NVLink peer memory, one persistent kernel per GPU); bit-identical
+  int num_gpus = 1;
   void validate() const;
 };
 

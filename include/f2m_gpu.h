@@ -102,7 +102,8 @@ typedef struct {
   int max_degree;
   int64_t sell_slots; /* padded SELL-32 slot count (>= 2m) */
   int sweep_ctas;      /* CTAs of the persistent sweep kernel (<= SM count) */
-  int sweep_variant;   /* 1 = grid-barrier kernel, 2 = neighbour-synchronised (smem-staged), 3 = 2 + smem-resident slots */
+  int sweep_variant;   /* 1 = grid-barrier kernel (k_gdp_sweep), 2 = persistent LL kernel streaming the slots
+                          (k_gdp_sweep5<.., false, ..>), 3 = persistent LL kernel, slots resident in smem */
   int max_local;       /* max over CTAs of own + halo nodes (v2 local index space) */
   int64_t max_cta_slots; /* max over CTAs of padded slots */
   int64_t smem_bytes;  /* dynamic shared memory of the v2 kernel */
@@ -131,6 +132,11 @@ typedef struct {            /* EngineConfig, dual.hpp:29-40 */
   int update;               /* 0 = midpoint, 1 = paper-difference */
   int init;                 /* 0 = local-midpoint, 1 = zero */
   int threads;              /* accepted for API parity; the device decides its own grid */
+  int num_gpus;             /* <= 1: one GPU (the graph's). > 1: solve_duals' Jacobi sweeps run on
+                               that many GPUs from the calling thread (multi.cu: the graph is
+                               replicated and partitioned across them, halo multipliers move over
+                               NVLink peer memory inside one persistent kernel per GPU); clamped to
+                               the graph's 32-node slice count. Results are bit-identical. */
 } f2m_engine_config;
 
 typedef struct {            /* ConvergenceReport, dual.hpp:48-54 */
@@ -338,6 +344,19 @@ int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_config* cfg, int
                            unsigned long long* d_cmax, unsigned long long* const* d_cmax_peers, double threshold,
                            int max_sweeps, void* d_ctl, void* stream);
 int f2m_sweep_multi_result(const void* d_ctl, int* sweeps, int* converged, double* final_max, int* out_buffer);
+/* Peer-memory stores rank r issues per sweep: LL words of its boundary multipliers into the other
+ * ranks that read them, and its CTAs' sweep maxima into the other ranks' max rings (16 B each). */
+int f2m_sweep_multi_traffic(const f2m_graph* g, int rank, int world, int64_t* remote_ll_stores,
+                            int64_t* remote_max_stores);
+
+/* ---- single-process multi-GPU (f2m_engine_config.num_gpus > 1) ------------------------------
+ * Devices of rank 0..num_gpus-1 (default: the graph's device and the next num_gpus-1, modulo the
+ * device count). A device may repeat: those ranks then share its SMs (test configurations on one
+ * GPU). count = 0 restores the default. */
+int f2m_set_gpu_list(const int* devices, int count);
+/* Facts of the most recent num_gpus > 1 solve on g: ranks, total partition CTAs, and whether the
+ * per-CTA slot data is shared-memory resident (else streamed from L2/HBM each sweep). */
+int f2m_multi_gpu_info(const f2m_graph* g, int* world, int* partition_ctas, int* resident);
 
 /* ---- instrumentation (bench.py / tests) ----------------------------------------------- */
 /* Number of kernels this library launched since load (all entry points). */

@@ -686,7 +686,9 @@ void finalize_topology(Topology& t) {
   t.nslices = (n + 31) / 32;
   // one SM stays free for the v5 kernel's convergence-master CTA
   const int sms = sweep_grid_ctas(t.dev);
-  const int target = g_sweep_partition > 0 ? g_sweep_partition : (sms > 1 ? sms - 1 : 1);
+  const int target = t.partition_override > 0 ? t.partition_override
+                     : g_sweep_partition > 0   ? g_sweep_partition
+                                               : (sms > 1 ? sms - 1 : 1);
   t.sweep_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(target, t.nslices));
   const int G = t.sweep_ctas;
   t.cta_lo.alloc(G + 1, s);

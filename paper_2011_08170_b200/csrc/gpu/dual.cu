@@ -1658,9 +1658,20 @@ void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const 
   rep.sweeps = 0;
   rep.final_max_abs_delta = INFINITY;
   DBuf<double>* result = &l0;
+  // EngineConfig::num_gpus: the Jacobi sweeps on several GPUs (multi.cu), clamped to the slices
+  const int64_t nsl = ((int64_t)t.n + 31) / 32;
+  const int world = (int)std::max<int64_t>(1, std::min<int64_t>(cfg.num_gpus, nsl));
   if (cfg.max_sweeps > 0) {
     check_degree(g, cfg.b);
-    if (cfg.mode == 0) {
+    if (cfg.mode == 0 && world > 1 && !g.allpairs) {
+      if (init_err) {  // lambda_0 (l0) goes to the replicas: collect the init's watchdog flag first
+        F2M_CUDA(cudaStreamSynchronize(s));
+        if (*init_err) throw Error(F2M_E_TIMEOUT, "initial-state kernel: dependency wait watchdog fired");
+      }
+      solve_duals_multi(g, cfg, world, l0.get(), l1, rep);
+      F2M_CUDA(cudaSetDevice(t.dev));
+      result = &l1;
+    } else if (cfg.mode == 0) {
       SweepResult r = run_jacobi(g, cfg, l0.get(), l1.get(), cfg.max_sweeps, threshold, nullptr,
                                  defer ? cfg.eps : 0.0);
       rep.sweeps = r.sweeps;
@@ -1808,6 +1819,13 @@ extern "C" int f2m_solve_duals(const f2m_graph* g, const f2m_engine_config* cfg,
   });
 }
 
+namespace f2mgpu {
+void note_sweep_kernel(double ms, int sweeps) {
+  g_last_sweep_ms = ms;
+  g_last_sweep_count = sweeps;
+}
+}  // namespace f2mgpu
+
 extern "C" const char* f2m_last_sweep_kernel_desc(void) { return g_last_sweep_desc.c_str(); }
 
 extern "C" int f2m_last_sweep_kernel_ms(double* ms, int* sweeps) {
@@ -1855,6 +1873,49 @@ __global__ void k_ll_mask(int G, int gp, const int32_t* __restrict__ halo_off, c
   for (int h = halo_off[c] + threadIdx.x; h < halo_off[c + 1]; h += blockDim.x) atomicOr(&mask[halo_pub[h]], bit);
 }
 }  // namespace f2mgpu
+
+namespace f2mgpu {
+// per-sweep remote LL stores of rank r: every boundary node of r's CTAs is stored into each OTHER
+// rank whose CTAs read it (popcount of its rank mask without bit r)
+__global__ void k_ll_remote(int G, int gp, int rank, const int32_t* __restrict__ boff,
+                            const uint32_t* __restrict__ mask, unsigned long long* __restrict__ count) {
+  const int lo = boff[rank * gp], hi = boff[min(G, (rank + 1) * gp)];
+  unsigned long long local = 0;
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
+    local += __popc(mask[i] & ~(1u << rank));
+  if (local) atomicAdd(count, local);
+}
+}  // namespace f2mgpu
+
+extern "C" int f2m_sweep_multi_traffic(const f2m_graph* g, int rank, int world, int64_t* remote_ll_stores,
+                                       int64_t* remote_max_stores) {
+  return f2mgpu::guard([&] {
+    using namespace f2mgpu;
+    const Topology& t = *g->topo;
+    if (world < 1 || !t.v2 || t.sweep_ctas % world) throw Error(F2M_E_ARGUMENT, "multi sweep: bad partition");
+    if (rank < 0 || rank >= world) throw Error(F2M_E_INDEX, "multi sweep: rank outside [0, world)");
+    if (world > 32) throw Error(F2M_E_ARGUMENT, "multi sweep: at most 32 ranks");
+    F2M_CUDA(cudaSetDevice(t.dev));
+    cudaStream_t s = t.stream;
+    const int G = t.sweep_ctas, Gp = G / world;
+    const int nb = std::max(t.nboundary, 1);
+    DBuf<uint32_t> mask((size_t)nb, s);
+    DBuf<unsigned long long> cnt(1, s);
+    F2M_CUDA(cudaMemsetAsync(mask.get(), 0, mask.bytes(), s));
+    F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), s));
+    if (G > 0) {
+      k_ll_mask<<<G, 128, 0, s>>>(G, Gp, t.halo_off.get(), t.halo_pub.get(), mask.get());
+      launched("ll_mask");
+      k_ll_remote<<<64, 256, 0, s>>>(G, Gp, rank, t.boff.get(), mask.get(), cnt.get());
+      launched("ll_remote");
+    }
+    unsigned long long h = 0;
+    F2M_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaStreamSynchronize(s));
+    *remote_ll_stores = (int64_t)h;
+    *remote_max_stores = (int64_t)Gp * (world - 1);
+  });
+}
 
 extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_config* cfg, int rank, int world,
                                       double* d_ring, unsigned long long* d_ll,

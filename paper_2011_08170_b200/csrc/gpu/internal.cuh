@@ -159,8 +159,11 @@ struct Topology {
   int max_local = 0;           // max over CTAs of own + halo
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
+  int partition_override = 0;  // > 0: partition CTA count for finalize_topology (multi-GPU replicas)
   ~Topology();
 };
+
+struct MultiPlan;  // multi.cu: per-graph replicas + rings of the single-process multi-GPU solve
 
 }  // namespace f2mgpu
 
@@ -180,6 +183,9 @@ struct f2m_graph {
   f2mgpu::DBuf<double2> pts_pos;
   int rounded = 0;
   bool allpairs = false;
+  // num_gpus > 1 solves: the graph replicated onto every GPU (partitioned into world x Gp CTAs)
+  // and the rings of the multi-rank sweep kernel, built on first use and kept with the graph
+  mutable std::shared_ptr<f2mgpu::MultiPlan> multi;
 };
 
 namespace f2mgpu {
@@ -255,6 +261,12 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
                        double* d_lam1, int max_sweeps, double threshold, double* d_record,
                        double defer_eps = 0.0);
 void validate_engine(const f2m_engine_config& cfg);
+// device time / sweeps of the most recent persistent sweep launch (f2m_last_sweep_kernel_ms)
+void note_sweep_kernel(double ms, int sweeps);
+// multi.cu: solve_duals on world_req GPUs from this host thread (EngineConfig::num_gpus > 1);
+// d_lam_out: lambda in g's position order; rep: sweeps / converged / final max (no dual value)
+void solve_duals_multi(const f2m_graph& g, const f2m_engine_config& cfg, int world_req, const double* d_init,
+                       DBuf<double>& d_lam_out, f2m_convergence_report& rep);
 // h_dual_async: see dual_objective_device (rep.dual_value is then left NaN for the caller)
 void solve_duals_device(const f2m_graph& g, const f2m_engine_config& cfg, const double* d_init,
                         DBuf<double>& d_lam_out, f2m_convergence_report& rep, double* h_dual_async = nullptr);

@@ -176,6 +176,7 @@ static f2m_engine_config to_c(const EngineConfig& c) {
   r.update = c.update == UpdateRule::kPaperDifference ? 1 : 0;
   r.init = c.init == DualInit::kZero ? 1 : 0;
   r.threads = c.threads;
+  r.num_gpus = c.num_gpus;
   return r;
 }
 

@@ -209,8 +209,10 @@ PYBIND11_MODULE(_f2m, m) {
   m.def(
       "solve_duals",
       [](const f2m::Graph& graph, int b, double eta, double eps, int max_sweeps, const std::string& mode,
-         const std::string& update, const std::string& init, int threads, std::optional<f2m::DualState> initial) {
-        const f2m::EngineConfig config = engine_config(b, eta, eps, max_sweeps, mode, update, init, threads);
+         const std::string& update, const std::string& init, int threads, std::optional<f2m::DualState> initial,
+         int num_gpus) {
+        f2m::EngineConfig config = engine_config(b, eta, eps, max_sweeps, mode, update, init, threads);
+        config.num_gpus = num_gpus;
         std::pair<f2m::DualState, f2m::ConvergenceReport> res;
         {
           py::gil_scoped_release release;
@@ -224,7 +226,7 @@ PYBIND11_MODULE(_f2m, m) {
       },
       py::arg("graph"), py::arg("b") = 2, py::arg("eta") = 0.5, py::arg("eps") = 1e-9, py::arg("max_sweeps") = 20000,
       py::arg("mode") = "jacobi", py::arg("update") = "midpoint", py::arg("init") = "local-midpoint",
-      py::arg("threads") = 0, py::arg("initial") = py::none());
+      py::arg("threads") = 0, py::arg("initial") = py::none(), py::arg("num_gpus") = 1);
 
   // --- extensions: the sweep-level entry points the reference keeps C++-only (dual.hpp:66-90)
   m.def(
@@ -304,10 +306,11 @@ PYBIND11_MODULE(_f2m, m) {
   m.def(
       "full_solve",
       [](const f2m::Instance& instance, int k, double eta, double eps, int max_sweeps, const std::string& mode,
-         double tol, int max_restarts, std::uint64_t seed, int threads) {
+         double tol, int max_restarts, std::uint64_t seed, int threads, int num_gpus) {
         f2m::RunConfig config;
         config.k = k;
         config.engine = engine_config(2, eta, eps, max_sweeps, mode, "midpoint", "local-midpoint", threads);
+        config.engine.num_gpus = num_gpus;
         config.tol = tol;
         config.max_restarts = max_restarts;
         config.seed = seed;
@@ -325,15 +328,16 @@ PYBIND11_MODULE(_f2m, m) {
       },
       py::arg("instance"), py::arg("k") = 20, py::arg("eta") = 0.5, py::arg("eps") = 1e-9,
       py::arg("max_sweeps") = 20000, py::arg("mode") = "jacobi", py::arg("tol") = 0.0, py::arg("max_restarts") = 5,
-      py::arg("seed") = 0, py::arg("threads") = 0);
+      py::arg("seed") = 0, py::arg("threads") = 0, py::arg("num_gpus") = 1);
 
   m.def(
       "full_solve_graph",
       [](const f2m::Graph& graph, int k, double eta, double eps, int max_sweeps, const std::string& mode, double tol,
-         int max_restarts, std::uint64_t seed, int threads) {
+         int max_restarts, std::uint64_t seed, int threads, int num_gpus) {
         f2m::RunConfig config;
         config.k = k;
         config.engine = engine_config(2, eta, eps, max_sweeps, mode, "midpoint", "local-midpoint", threads);
+        config.engine.num_gpus = num_gpus;
         config.tol = tol;
         config.max_restarts = max_restarts;
         config.seed = seed;
@@ -351,7 +355,7 @@ PYBIND11_MODULE(_f2m, m) {
       },
       py::arg("graph"), py::arg("k") = 20, py::arg("eta") = 0.5, py::arg("eps") = 1e-9, py::arg("max_sweeps") = 20000,
       py::arg("mode") = "jacobi", py::arg("tol") = 0.0, py::arg("max_restarts") = 5, py::arg("seed") = 0,
-      py::arg("threads") = 0);
+      py::arg("threads") = 0, py::arg("num_gpus") = 1);
 
   // --- C-ABI pipeline entry points with array I/O (benchmark e2e / device-resident paths)
   m.def(
@@ -471,6 +475,14 @@ PYBIND11_MODULE(_f2m, m) {
            py::arg("peer_board"), py::arg("lam_a"), py::arg("lam_b"), py::arg("threshold"), py::arg("max_sweeps"),
            py::arg("ctas"), py::arg("ctl"), py::arg("stream") = 0);
   m.def("set_sweep_partition", [](int ctas) { f2m_set_sweep_partition(ctas); }, py::arg("ctas"));
+  m.def("set_gpu_list", [](const std::vector<int>& devices) {
+    f2m::check(f2m_set_gpu_list(devices.data(), static_cast<int>(devices.size())));
+  }, py::arg("devices"));
+  m.def("multi_gpu_info", [](const f2m::Graph& graph) {
+    int w = 0, p = 0, r = 0;
+    f2m::check(f2m_multi_gpu_info(graph.handle(), &w, &p, &r));
+    return py::dict(py::arg("world") = w, py::arg("partition_ctas") = p, py::arg("resident") = (bool)r);
+  }, py::arg("graph"));
   m.def("sweep_multi_info", [](const f2m::Graph& graph, int rank, int world) {
     int gt = 0, res = 0, b = 0, e = 0;
     std::int64_t llw = 0, cmw = 0;
@@ -479,6 +491,12 @@ PYBIND11_MODULE(_f2m, m) {
                     py::arg("cmax_words") = cmw, py::arg("begin") = b, py::arg("end") = e);
   });
   m.def("sweep_multi_ctl_bytes", []() { return f2m_sweep_multi_ctl_bytes(); });
+  m.def("sweep_multi_traffic", [](const f2m::Graph& graph, int rank, int world) {
+    std::int64_t ll = 0, mx = 0;
+    f2m::check(f2m_sweep_multi_traffic(graph.handle(), rank, world, &ll, &mx));
+    return py::dict(py::arg("remote_ll_stores") = ll, py::arg("remote_max_stores") = mx,
+                    py::arg("bytes_per_sweep") = 16 * (ll + mx));
+  }, py::arg("graph"), py::arg("rank"), py::arg("world"));
   m.def(
       "sweep_multi_launch",
       [](const f2m::Graph& graph, int b, double eta, const std::string& update, int rank, int world,

@@ -609,7 +609,14 @@ class ShardedResident:
     plain device memory for LocalComm ranks, which then run concurrently on one GPU). No barrier,
     host work or collective per sweep; bit-identical to one GPU.
 
-    ShardedResident(inst, k, comm).run(threshold, max_sweeps) -> (lambda in node-id order, report)."""
+    ShardedResident(inst, k, comm).run(threshold, max_sweeps) -> (lambda in node-id order, report).
+
+    In-process ranks (LocalComm) run `world` cooperative launches on separate streams of ONE GPU
+    that spin on each other's LL words. CUDA guarantees co-residency only inside one cooperative
+    grid, so this form is a test configuration: it relies on the launches running concurrently
+    (they fit: world x (Gp + 1) CTAs <= SMs) and the 20 s in-kernel watchdog turns a serialised
+    schedule into an error instead of a hang. Production multi-GPU runs one process per GPU
+    (TorchDistComm) or one host thread over several GPUs (EngineConfig::num_gpus, multi.cu)."""
 
     def __init__(self, inst, k: int, comm, b: int = 2, eta: float = 0.5, update: str = "midpoint",
                  init: str = "local-midpoint", ctas_per_rank: int = 0):
@@ -641,24 +648,11 @@ class ShardedResident:
         self.info = {r: _f2m.sweep_multi_info(g, r, world) for r in self.ranks}
         i0 = next(iter(self.info.values()))
         self.g_total = i0["g_total"]
-        llw, cmw = int(i0["ll_words"]), int(i0["cmax_words"])
+        self.resident = bool(i0["resident"])
+        self._words = (int(i0["ll_words"]), int(i0["cmax_words"]))
+        self.connected = False
         if local:
-            self.ll = {r: torch.zeros(llw, dtype=torch.int64, device=dev) for r in self.ranks}
-            self.cmax = {r: torch.zeros(cmw, dtype=torch.int64, device=dev) for r in self.ranks}
-            ll_ptrs = [self.ll[r].data_ptr() for r in range(world)]
-            cm_ptrs = [self.cmax[r].data_ptr() for r in range(world)]
-        else:
-            import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm_mem
-
-            group = comm.group if comm.group is not None else dist.group.WORLD
-            lb = symm_mem.empty(llw, dtype=torch.int64, device=dev)
-            cb = symm_mem.empty(cmw, dtype=torch.int64, device=dev)
-            self._handles = (symm_mem.rendezvous(lb, group), symm_mem.rendezvous(cb, group))
-            self.ll, self.cmax = {comm.rank: lb}, {comm.rank: cb}
-            ll_ptrs, cm_ptrs = list(self._handles[0].buffer_ptrs), list(self._handles[1].buffer_ptrs)
-        self.ll_peers = torch.tensor(ll_ptrs, dtype=torch.int64, device=dev)
-        self.cmax_peers = torch.tensor(cm_ptrs, dtype=torch.int64, device=dev)
+            self.connect()
         self.lam0 = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
         if n > 0:
             _f2m.initial_state_positions(g, self.lam0.data_ptr(), b, init, torch.cuda.current_stream(dev).cuda_stream)
@@ -667,7 +661,36 @@ class ShardedResident:
                     for r in self.ranks}
         self.streams = {r: torch.cuda.Stream(dev) for r in self.ranks}
 
+    def connect(self) -> None:
+        """Allocate the LL / max rings and exchange their addresses. Across processes this is a
+        collective (torch symmetric-memory rendezvous over comm's group): every rank must reach
+        it, so callers that can fail per rank agree first (bench.py `_agree`); everything before
+        it in __init__ is rank-local."""
+        if self.connected:
+            return
+        dev, world = self.dev, self.world
+        llw, cmw = self._words
+        if self.local:
+            self.ll = {r: torch.zeros(llw, dtype=torch.int64, device=dev) for r in self.ranks}
+            self.cmax = {r: torch.zeros(cmw, dtype=torch.int64, device=dev) for r in self.ranks}
+            ll_ptrs = [self.ll[r].data_ptr() for r in range(world)]
+            cm_ptrs = [self.cmax[r].data_ptr() for r in range(world)]
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            group = self.comm.group if self.comm.group is not None else dist.group.WORLD
+            lb = symm_mem.empty(llw, dtype=torch.int64, device=dev)
+            cb = symm_mem.empty(cmw, dtype=torch.int64, device=dev)
+            self._handles = (symm_mem.rendezvous(lb, group), symm_mem.rendezvous(cb, group))
+            self.ll, self.cmax = {self.comm.rank: lb}, {self.comm.rank: cb}
+            ll_ptrs, cm_ptrs = list(self._handles[0].buffer_ptrs), list(self._handles[1].buffer_ptrs)
+        self.ll_peers = torch.tensor(ll_ptrs, dtype=torch.int64, device=dev)
+        self.cmax_peers = torch.tensor(cm_ptrs, dtype=torch.int64, device=dev)
+        self.connected = True
+
     def launch(self, threshold: float, max_sweeps: int, ev_start=None, ev_end=None) -> None:
+        self.connect()
         for r in self.ranks:
             self.ll[r].zero_()
             self.cmax[r].zero_()
@@ -691,7 +714,9 @@ class ShardedResident:
         if ev_end is not None:
             ev_end.record(cur)
 
-    def collect(self):
+    def collect_local(self):
+        """This process's ranks' results (no collective): (lambda in position order with this
+        process's ranges filled, result dict). Raises on a watchdog abort."""
         n = self.n
         lam_pos = torch.zeros(max(n, 1), dtype=torch.float64, device=self.dev)
         res = None
@@ -701,26 +726,44 @@ class ShardedResident:
             res = rr
             lo, hi = self.info[r]["begin"], self.info[r]["end"]
             lam_pos[lo:hi] = self.rings[r][rr["out_buffer"]][lo:hi]
+        return lam_pos, res
+
+    def gather(self, lam_pos):
+        """Every rank's owned range into every rank's vector (collective across processes)."""
         if not self.local:  # ranks own contiguous position ranges of different lengths: pad, gather
             if not hasattr(self, "_width"):  # the longest rank range (identical topology on every rank)
                 spans = [self._f2m.sweep_multi_info(self.graph, q, self.world) for q in range(self.world)]
                 self._width = max(1, max(x["end"] - x["begin"] for x in spans))
             lo, hi = self.info[self.comm.rank]["begin"], self.info[self.comm.rank]["end"]
             gather_ranges(self.comm, lam_pos, lo, hi, self._width)
-        return lam_pos, res
+        return lam_pos
+
+    def collect(self):
+        lam_pos, res = self.collect_local()
+        return self.gather(lam_pos), res
+
+    def to_ids(self, lam_pos):
+        """Position-order multipliers -> node-id order (host numpy array)."""
+        ids = torch.empty(max(self.n, 1), dtype=torch.float64, device=self.dev)
+        if self.n > 0:
+            self._f2m.positions_to_ids(self.graph, lam_pos.data_ptr(), ids.data_ptr(),
+                                       torch.cuda.current_stream(self.dev).cuda_stream)
+        return ids[:self.n].cpu().numpy()
+
+    def peer_bytes_per_sweep(self):
+        """Peer-memory (NVLink) bytes each rank stores into other ranks per sweep: LL words of the
+        boundary multipliers other ranks read + the CTA maxima, 16 B each (max over ranks)."""
+        return max(self._f2m.sweep_multi_traffic(self.graph, q, self.world)["bytes_per_sweep"]
+                   for q in range(self.world))
 
     def run(self, threshold: float, max_sweeps: int):
         self.launch(threshold, max_sweeps)
         torch.cuda.synchronize(self.dev)
         lam_pos, res = self.collect()
-        ids = torch.empty(max(self.n, 1), dtype=torch.float64, device=self.dev)
-        if self.n > 0:
-            self._f2m.positions_to_ids(self.graph, lam_pos.data_ptr(), ids.data_ptr(),
-                                       torch.cuda.current_stream(self.dev).cuda_stream)
         report = {"converged": res["converged"], "sweeps": res["sweeps"],
                   "final_max_abs_delta": res["final_max_abs_delta"], "world": self.world, "g_total": self.g_total,
                   "exchange": "resident"}
-        return ids[:self.n].cpu().numpy(), report
+        return self.to_ids(lam_pos), report
 
 
 def solve_duals_resident(inst, k: int, comm=None, eps: float = 1e-9, max_sweeps: int = 20000, **kw):
