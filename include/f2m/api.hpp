@@ -174,6 +174,13 @@ std::pair<DualState, ConvergenceReport> solve_duals(
     const Graph& graph, const EngineConfig& config,
     const std::optional<DualState>& initial = std::nullopt);
 DualState make_initial_state(const Graph& graph, const EngineConfig& config);
+// Internal entry points reusing a caller-owned pool (dual.hpp:83-87). The pool is accepted for
+// source compatibility and not used: the sweep and the objective run on the GPU. delta_scratch
+// receives every node's delta from the frozen snapshot, as the reference leaves it.
+class ThreadPool;  // f2m/parallel.hpp
+SweepStats jacobi_sweep(const Graph& graph, DualState& state, const EngineConfig& config, ThreadPool& pool,
+                        std::vector<double>& delta_scratch);
+double dual_objective_pooled(const Graph& graph, const DualState& state, int b, ThreadPool* pool);
 /// `count` Jacobi sweeps in one persistent kernel; per-sweep max |delta| (B200 extension).
 std::vector<double> jacobi_sweeps(const Graph& graph, DualState& state, const EngineConfig& config,
                                   int count, double* dual_value = nullptr);

@@ -83,6 +83,12 @@ int f2m_knn_build(int n, const double* xy, int rounded, int k, f2m_graph** out);
 /* Same, with the points already resident in device memory (d_xy, 2n doubles). */
 int f2m_knn_build_device(int n, const double* d_xy, int rounded, int k, f2m_graph** out);
 
+/* generate_instance (instance.cpp:143-157) on the device: the n uniform points of the SplitMix64
+ * stream seeded `seed` in [0, box)^2 written to d_xy (2n doubles, x then y per point), bit-identical
+ * to the host generator (counter-based: draw j of the stream is computed directly). Stream-ordered
+ * on `stream` (NULL = legacy default), no synchronisation. */
+int f2m_generate_instance_device(int n, uint64_t seed, double box, double* d_xy, void* stream);
+
 /* Graph::with_costs (graph.cpp:53-65): same topology, new costs and mean cost. */
 int f2m_graph_with_costs(const f2m_graph* g, const double* cost, f2m_graph** out);
 
@@ -159,6 +165,11 @@ int f2m_initial_state(const f2m_graph* g, const f2m_engine_config* cfg, double* 
  * g(lambda) after the last sweep. F2M_E_DEGREE if some degree <= b. */
 int f2m_jacobi_sweeps(const f2m_graph* g, const f2m_engine_config* cfg, double* lambda_inout,
                       int count, double* max_abs_delta, double* dual_value);
+
+/* Phase 1 of jacobi_sweep (dual.cpp:138-152) alone: delta[v] for every node from the frozen
+ * lambda (smallest_adjusted + delta_for with cfg->b / cfg->update); the pooled jacobi_sweep
+ * overload's delta scratch (dual.hpp:83-85). F2M_E_DEGREE if some degree <= b. */
+int f2m_jacobi_deltas(const f2m_graph* g, const f2m_engine_config* cfg, const double* lambda, double* delta);
 
 /* `count` Gauss-Seidel sweeps (gauss_seidel_sweep, dual.cpp:175-192), in place. */
 int f2m_gauss_seidel_sweeps(const f2m_graph* g, const f2m_engine_config* cfg,

@@ -1534,6 +1534,18 @@ __global__ void k_node_delta(int p, int d, const int64_t* __restrict__ sptr,
   if (threadIdx.x == 0) *out = r;
 }
 
+// phase 1 of jacobi_sweep (dual.cpp:138-152) alone: every node's delta from the frozen lambda,
+// one warp per node (the pooled jacobi_sweep overload's delta scratch)
+template <int B>
+__global__ void k_all_deltas(int n, const int32_t* __restrict__ deg, const int64_t* __restrict__ sptr,
+                             const int32_t* __restrict__ scol, const double* __restrict__ scost,
+                             const double* lam, int update, double* __restrict__ out) {
+  const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (p >= n) return;
+  const double r = row_delta_warp<B>(p, deg[p], sptr, scol, scost, lam, update);
+  if ((threadIdx.x & 31) == 0) out[p] = r;
+}
+
 // ---------------------------------------------------------------- dual objective
 // Terms of the dual objective in the reference's accumulation order: lambda[v] for the node
 // chunks (dual.cpp:96-100) and min(v_e, 0) for the edge chunks, v_e = (c - l_u) - l_v
@@ -1760,6 +1772,28 @@ extern "C" int f2m_gauss_seidel_sweeps(const f2m_graph* g, const f2m_engine_conf
     }
     if (dual_value) *dual_value = dual_objective_device(*g, l0.get(), cfg->b);
     download_lambda(*g, l0.get(), lambda_inout);
+  });
+}
+
+extern "C" int f2m_jacobi_deltas(const f2m_graph* g, const f2m_engine_config* cfg, const double* lambda,
+                                 double* delta) {
+  return guard([&] {
+    validate_engine(*cfg);
+    const Topology& t = *g->topo;
+    F2M_CUDA(cudaSetDevice(t.dev));
+    if (t.n == 0) return;
+    check_degree(*g, cfg->b);
+    cudaStream_t s = t.stream;
+    DBuf<double> l0(t.n, s), d0(t.n, s);
+    upload_lambda(*g, lambda, l0.get());
+    const unsigned blocks = grid_for((int64_t)t.n * 32, 256);
+    switch (cfg->b) {
+#define F2M_AD(BB) case BB: k_all_deltas<BB><<<blocks, 256, 0, s>>>(t.n, t.deg.get(), t.sptr.get(), t.scol.get(), g->scost.get(), l0.get(), cfg->update, d0.get()); break;
+      F2M_AD(1) F2M_AD(2) F2M_AD(3) F2M_AD(4) F2M_AD(5) F2M_AD(6) F2M_AD(7) F2M_AD(8)
+#undef F2M_AD
+    }
+    launched("all_deltas");
+    download_lambda(*g, d0.get(), delta);
   });
 }
 

@@ -492,6 +492,27 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
 
 using namespace f2mgpu;
 
+namespace f2mgpu {
+// generate_instance (instance.cpp:143-157): point i takes draws 2i (x) and 2i+1 (y) of the
+// SplitMix64 stream seeded `seed`, each next_double() * box (one rounded product: bit-exact).
+__global__ void k_generate_uniform(int n, uint64_t seed, double box, double* __restrict__ xy) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= 2 * (int64_t)n) return;
+  xy[j] = dmul(splitmix64_double_at(seed, (uint64_t)j), box);
+}
+}  // namespace f2mgpu
+
+extern "C" int f2m_generate_instance_device(int n, uint64_t seed, double box, double* d_xy, void* stream) {
+  return guard([&] {
+    if (n < 1) throw Error(F2M_E_ARGUMENT, "generate_instance: n must be >= 1");
+    if (!(box > 0.0)) throw Error(F2M_E_ARGUMENT, "generate_instance: box must be > 0");
+    F2M_CUDA(cudaSetDevice(current_device()));
+    k_generate_uniform<<<grid_for(2 * (int64_t)n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, seed, box,
+                                                                                                     d_xy);
+    launched("generate_uniform");
+  });
+}
+
 extern "C" int f2m_knn_build_device(int n, const double* d_xy, int rounded, int k, f2m_graph** out) {
   return guard([&] {
     *out = nullptr;

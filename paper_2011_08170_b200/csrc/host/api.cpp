@@ -223,6 +223,21 @@ SweepStats jacobi_sweep(const Graph& graph, DualState& state, const EngineConfig
   return st;
 }
 
+SweepStats jacobi_sweep(const Graph& graph, DualState& state, const EngineConfig& config, ThreadPool& /*pool*/,
+                        std::vector<double>& delta_scratch) {
+  config.validate();
+  need(graph);
+  check_size(graph, state, "jacobi_sweep");
+  const f2m_engine_config c = to_c(config);
+  delta_scratch.resize(static_cast<size_t>(graph.node_count()));
+  if (graph.node_count() > 0) check(f2m_jacobi_deltas(graph.handle(), &c, state.lambda.data(), delta_scratch.data()));
+  return jacobi_sweep(graph, state, config);
+}
+
+double dual_objective_pooled(const Graph& graph, const DualState& state, int b, ThreadPool* /*pool*/) {
+  return dual_objective(graph, state, b);
+}
+
 SweepStats gauss_seidel_sweep(const Graph& graph, DualState& state, const EngineConfig& config) {
   config.validate();
   need(graph);

@@ -474,6 +474,11 @@ PYBIND11_MODULE(_f2m, m) {
            py::arg("send_dst"), py::arg("n_send"), py::arg("peer_recv"), py::arg("peer_nrecv"), py::arg("board"),
            py::arg("peer_board"), py::arg("lam_a"), py::arg("lam_b"), py::arg("threshold"), py::arg("max_sweeps"),
            py::arg("ctas"), py::arg("ctl"), py::arg("stream") = 0);
+  m.def("generate_instance_device", [](int n, std::uint64_t seed, double box, std::uintptr_t d_xy,
+                                        std::uintptr_t stream) {
+    f2m::check(f2m_generate_instance_device(n, seed, box, reinterpret_cast<double*>(d_xy),
+                                            reinterpret_cast<void*>(stream)));
+  }, py::arg("n"), py::arg("seed"), py::arg("box"), py::arg("d_xy"), py::arg("stream") = 0);
   m.def("set_sweep_partition", [](int ctas) { f2m_set_sweep_partition(ctas); }, py::arg("ctas"));
   m.def("set_gpu_list", [](const std::vector<int>& devices) {
     f2m::check(f2m_set_gpu_list(devices.data(), static_cast<int>(devices.size())));
