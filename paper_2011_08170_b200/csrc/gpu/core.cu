@@ -47,7 +47,7 @@ Topology::~Topology() {
     cudaSetDevice(dev);
     eu.release(); ev.release(); perm.release(); iperm.release(); deg.release();
     sptr.release(); swidth.release(); scol.release(); seid.release(); cta_lo.release();
-    halo_off.release(); halo.release(); slidx.release(); nbr_off.release(); nbr.release();
+    halo_off.release(); halo.release(); slidx.release();
     cta_int_hi.release(); cta_nint.release(); boff.release(); halo_pub.release();
     sdest.release(); row_nhalo.release();
     cudaStreamSynchronize(stream);
@@ -423,22 +423,6 @@ __global__ void k_halo_last(int n, int64_t nslices, const int64_t* __restrict__ 
   if (p < n) nhalo[p] = (uint8_t)min(nh, 255);
 }
 
-// CTA adjacency: owner of every halo node (halo sorted by (cta, q); owners are monotone in q)
-__global__ void k_nbr_keys(int ctas, const int32_t* __restrict__ hoff, const int32_t* __restrict__ halo,
-                           const int32_t* __restrict__ cos, uint64_t* __restrict__ keys) {
-  const int c = blockIdx.x;
-  for (int i = hoff[c] + threadIdx.x; i < hoff[c + 1]; i += blockDim.x)
-    keys[i] = ((uint64_t)(uint32_t)c << 32) | (uint32_t)cos[halo[i] >> 5];
-}
-
-__global__ void k_nbr_split(int64_t k, const uint64_t* __restrict__ keys, int32_t* __restrict__ nbr,
-                            int32_t* __restrict__ cnt) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= k) return;
-  nbr[i] = (int32_t)(keys[i] & 0xffffffffu);
-  atomicAdd(&cnt[keys[i] >> 32], 1);
-}
-
 // ---- LL exchange: boundary publication indices
 __global__ void k_boundary_counts(int ctas, int n, const int32_t* __restrict__ lo, const int32_t* __restrict__ nint,
                                   int32_t* __restrict__ cnt) {
@@ -588,37 +572,6 @@ static void build_local_index(Topology& t) {
                                                              t.slidx.get(), cos.get(), t.cta_lo.get(),
                                                              t.sdest.get(), t.row_nhalo.get());
     launched("halo_last");
-  }
-  // CTA adjacency (only the sweep-trace tooling reads it)
-  t.nbr_off.alloc(G + 1, s);
-  if (std::getenv("F2M_SWEEP_TRACE")) {
-    DBuf<uint64_t> nk(std::max<int64_t>(h, 1), s), nk2(std::max<int64_t>(h, 1), s);
-    int64_t k = 0;
-    if (h > 0) {
-      k_nbr_keys<<<G, 128, 0, s>>>(G, t.halo_off.get(), t.halo.get(), cos.get(), nk.get());
-      launched("nbr_keys");
-      size_t tmp = 0;
-      F2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, nk.get(), nk2.get(), nsel.get(), h, s));
-      DBuf<char> tb(tmp, s);
-      F2M_CUDA(cub::DeviceSelect::Unique(tb.get(), tmp, nk.get(), nk2.get(), nsel.get(), h, s));
-      launched("unique_nbr");
-      int64_t* hs = pinned_scratch();
-      F2M_CUDA(cudaMemcpyAsync(hs, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      F2M_CUDA(cudaStreamSynchronize(s));
-      k = hs[0];
-    }
-    t.nbr.alloc(std::max<int64_t>(k, 1), s);
-    DBuf<int32_t> cnt(G + 1, s);
-    F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (G + 1), s));
-    if (k > 0) {
-      k_nbr_split<<<grid_for(k, 256), 256, 0, s>>>(k, nk2.get(), t.nbr.get(), cnt.get());
-      launched("nbr_split");
-    }
-    size_t tmp = 0;
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.nbr_off.get(), G + 1, s));
-    DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.nbr_off.get(), G + 1, s));
-    launched("scan_nbr");
   }
   // LL publication indices (boundary nodes of each CTA, in position order)
   t.boff.alloc(G + 1, s);

@@ -298,13 +298,6 @@ __global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairs
   }
 }
 
-#define F2M_TRACE16(S, PH)                                                                  \
-  do {                                                                                      \
-    if (a.trace && (S) >= a.trace_first && (S) < a.trace_first + a.trace_count)             \
-      a.trace[(((size_t)((S) - a.trace_first) * (G + 1) + blockIdx.x) << 4) + (PH)] =        \
-          globaltimer_ns();                                                                 \
-  } while (0)
-
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -394,10 +387,9 @@ struct Sweep4Args {
   double* record;
   int lam_stride;
   const int32_t* __restrict__ sdest;     // v5: slot -> halo-last slot
-  const uint8_t* __restrict__ row_nhalo; // v5: halo slots per row
   unsigned poll_ns;          // v5: sync-warp back-off between unproductive halo polls
   int runahead;              // v5: stage the next sweep's halo while this sweep computes
-  int split;                 // sweep order: 4 boundary rows first, 6 the same with two lanes per boundary row (the defaults, by size), 3 boundary first with every warp at the halo hand-off, 1 interior first + own-CTA slots of boundary rows before the halo, 0 interior first
+  int pair_rows;             // two lanes per boundary row (small graphs: <= 256 rows per CTA)
   // deferred threshold (v5): defer_eps > 0 -> threshold = defer_eps * mean_cost, where the master
   // CTA computes mean_cost (sequential sum of cost[0..m) / m, graph.cpp:47-49) during the solve
   double defer_eps;
@@ -405,8 +397,6 @@ struct Sweep4Args {
   int64_t m;
   const double* __restrict__ approx_sum;
   double* mean_out;
-  unsigned long long* trace;
-  int trace_first, trace_count;
   // multi-GPU form (npeers > 0): this launch runs partition CTAs [cta_base, cta_base + gridDim.x -
   // 1) of g_total; every boundary multiplier and every CTA's sweep max is stored into all peers'
   // LL / max rings (peer memory), so each rank's master sees every CTA and issues the same verdicts
@@ -424,9 +414,9 @@ constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
 //  * two sync warps run up to one sweep AHEAD of the compute warps: the halo of sweep s+1 is
 //    polled and staged into the idle shared-memory region while sweep s is still computing, and
 //    handed over through named barriers (no CTA-wide barrier between the roles);
-//  * boundary rows (the only rows on the inter-CTA critical path) are computed by groups of L
-//    lanes (L = 1..8, as many as the CTA's boundary count allows) that split the row and merge
-//    their partial top-(B+1) lists with a bitonic merge, instead of one thread per row;
+//  * boundary rows (the only rows on the inter-CTA critical path) go first, one thread per row
+//    (two lanes per row with a shuffle merge of their top-(B+1) lists on small graphs), and only
+//    the warps that own them wait at the halo hand-off; the interior slices follow;
 //  * one CTA barrier per sweep: the stop decision for sweep s+1 is taken before barrier B of s.
 
 // warp max of non-negative doubles (|delta|) through their bit patterns (monotone for x >= 0):
@@ -472,8 +462,7 @@ __device__ __forceinline__ void master_sync(bool mean_warp_busy) {
 }
 
 __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__ cmax, int max_sweeps,
-                                         double threshold, double* record, unsigned long long* trace,
-                                         int trace_first, int trace_count, Sweep4Ctl* ctl, int G,
+                                         double threshold, double* record, Sweep4Ctl* ctl, int G,
                                          double defer_eps, const double* __restrict__ cost, int64_t m,
                                          const double* __restrict__ approx_sum, double* mean_out) {
   __shared__ unsigned long long m_max[kMasterWindow];
@@ -576,8 +565,6 @@ __device__ __noinline__ void sweep_master(const unsigned long long* __restrict__
           break;          // undecidable until the exact mean is in: retry next round
         }
         if (record) record[k] = g;
-        if (trace && k >= trace_first && k < trace_first + trace_count)
-          trace[(((size_t)(k - trace_first) * (G + 1) + G) << 4) + 0] = globaltimer_ns();
         m_g = g;
         if (below) {
           m_conv = 1;
@@ -650,8 +637,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   __shared__ int s_stop[2];
   __shared__ volatile int s_done;  // sweeps completed by the compute warps
   __shared__ volatile int s_exit;
-  __shared__ volatile int s_dummy;
-  __shared__ volatile int s_staged[2];
   __shared__ unsigned long long s_word;
   // CTAs 0..G-1 own the partition; the last CTA of the launch (alone on its SM) is the master.
   // Multi-GPU: this launch's CTAs are the partition CTAs cta_base.. of g_total.
@@ -660,8 +645,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int sync0 = nwarps - 2, ncw = nwarps - 2;
   if (blockIdx.x == gridDim.x - 1) {
-    sweep_master(a.cmax, a.max_sweeps, a.threshold, a.record, a.trace, a.trace_first, a.trace_count, ctl, G,
-                 a.defer_eps, a.cost, a.m, a.approx_sum, a.mean_out);
+    sweep_master(a.cmax, a.max_sweeps, a.threshold, a.record, ctl, G, a.defer_eps, a.cost, a.m, a.approx_sum,
+                 a.mean_out);
     return;
   }
   const int cthreads = ncw * 32;
@@ -675,13 +660,13 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // boundary row of this thread (per batch of cthreads rows): the rotation starts at the first
   // warp with the fewest interior slices, so boundary work lands on the least-loaded warps
   const int brow = (tid - ((s_int - s_lo) % ncw) * 32 + cthreads) % cthreads;
-  // split == 4: only the warps that own boundary rows (and the sync warps) meet at the halo
-  // hand-off; the others go straight to their interior rows
-  // two lanes per boundary row when the CTA has few of them (small graphs: at 10k the boundary
-  // chain dominates and idle lanes are plentiful; at 100k+ the interior rows need the lanes)
-  const bool pair_rows = RES && a.split == 6 && 2 * nbnd <= cthreads;
+  // only the warps that own boundary rows (and the sync warps) meet at the halo hand-off; the
+  // others go straight to their interior rows. Two lanes per boundary row when the CTA has few of
+  // them (small graphs: at 10k the boundary chain dominates and idle lanes are plentiful; at 100k+
+  // the interior rows need the lanes)
+  const bool pair_rows = RES && a.pair_rows && 2 * nbnd <= cthreads;
   const int bthreads = pair_rows ? 2 * nbnd : nbnd;  // threads (in rotated order) with boundary work
-  const bool own_bar = (a.split == 4 || a.split == 6) && bthreads <= cthreads;
+  const bool own_bar = bthreads <= cthreads;
   const int halo_bar = own_bar ? 64 + 32 * ((bthreads + 31) / 32) : cthreads + 64;
   const bool in_halo_bar = !own_bar || (brow & ~31) < bthreads;
   const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
@@ -694,13 +679,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
   // per-slice (slot offset, width) of this CTA: no global loads on the sweep path
   int2* slc = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(lid_s + (RES ? nslots : 0)) + 15) & ~uintptr_t(15));
-  uint8_t* nh_s = reinterpret_cast<uint8_t*>(slc + (s_hi - s_lo));  // halo slots per boundary row
   const double* __restrict__ gcost = a.scost + slot0;
   const uint16_t* __restrict__ glid = a.slidx + slot0;
   for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
   for (int i = tid; i < s_hi - s_lo; i += blockDim.x)
     slc[i] = make_int2((int)(a.sptr[s_lo + i] - slot0), a.swidth[s_lo + i]);
-  for (int i = tid; i < nbnd; i += blockDim.x) nh_s[i] = a.row_nhalo[p0 + bstart + i];
   if (RES) {
     for (int i = tid; i < nslots; i += blockDim.x) {  // rows stored own-first, halo-last
       const int d = (int)(a.sdest[slot0 + i] - slot0);
@@ -714,7 +697,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     s_stop[0] = s_stop[1] = -1;
     s_done = 0;
     s_exit = 0;
-    s_staged[0] = s_staged[1] = -1;
   }
   __syncthreads();
 
@@ -758,7 +740,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
               lam[own + base + lane + 64 * b] = ll_val(w0[b], w1[b]);
               pend &= ~(1u << b);
             }
-          if (sw == 0 && base == 0 && it == 0 && lane == 0) F2M_TRACE16(s, 1);
           // back off while nothing arrives: a spinning poller floods the SM's memory pipe that
           // the compute warps' shared-memory loads share
           if (__all_sync(0xffffffffu, pend == pend_before) && a.poll_ns) __nanosleep(a.poll_ns);
@@ -781,8 +762,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         }
       }
       __syncwarp();
-      if (sw == 0 && lane == 0) F2M_TRACE16(s, 2);
-      if (lane == 0) s_staged[sw] = s;
       // hand-off on a hardware barrier (compute warps sleep in bar.sync, no spinning); two ids
       // alternate so the run-ahead arrival for s+1 can never be counted towards sweep s
       named_arrive(3 + (s & 1), halo_bar);
@@ -791,11 +770,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     return;
   }
 
-  // ---- compute warps
-  const bool boundary_first = a.split >= 3;  // boundary rows (whole rows) before the interior
-  const bool split_mode = RES && a.split == 1;
+  // ---- compute warps. Boundary rows (the only rows other CTAs read) first: the halo of sweep s
+  // was published early in the neighbours' sweep s-1 (they too start with their boundary rows),
+  // so it is normally staged already; publish, then the interior rows overlap the neighbours'
+  // next exchange.
   for (int s = 0;; ++s) {
-    if (tid == 0) F2M_TRACE16(s, 0);
     double* lam = (RES && (s & 1)) ? regB : regA;
     double* lam_next = (s & 1) ? regA : regB;
     const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
@@ -805,63 +784,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       named_sync(2, cthreads);
     }
     double mx = 0.0;
-    long long ck0 = 0, ck1 = 0, ck2 = 0, ck3 = 0;
-    double pv[B + 1];
-#pragma unroll
-    for (int i = 0; i <= B; ++i) pv[i] = CUDART_INF;
-    auto interior_rows = [&]() {
-    // interior slices: one thread per node (throughput-bound phase)
-    for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
-      const int p = sl * 32 + lane;
-      if (p >= a.n) continue;
-      const int lp = p - p0;
-      const int2 sw2 = slc[sl - s_lo];
-      const int lb = sw2.x + lane;
-      const int w = sw2.y;
-      const double lv = lam[lp];
-      double sv[B + 1];
-#pragma unroll
-      for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-      int j = 0;
-      for (; j + 8 <= w; j += 8) {
-        int li[8];
-        double cs[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int idx = lb + 32 * (j + u);
-          li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
-          cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
-      }
-      for (; j < w; ++j) {
-        const int idx = lb + 32 * j;
-        const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
-        const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
-        topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
-      }
-      const double d = delta_of<B>(sv, a.update);
-      const double nl = dadd(lv, dmul(a.eta, d));
-      gout[p] = nl;
-      if (RES) lam_next[lp] = nl;
-      const double ad = fabs(d);
-      mx = mx < ad ? ad : mx;
-    }
-    };
-    auto halo_and_boundary_rows = [&]() {
     if (in_halo_bar) named_sync(3 + (s & 1), halo_bar);  // halo of sweep s staged
-    if (warp == 0 && lane == 0) {
-      F2M_TRACE16(s, 3);
-      if (a.trace && s >= a.trace_first && s < a.trace_first + a.trace_count)
-        a.trace[(((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4) + 9] =
-            (unsigned long long)(long long)(min(s_staged[0], s_staged[1]) - s);
-    }
-    ck0 = clock64();
-    // boundary rows, second pass: the halo slots (RES, first batch) or the whole row
+    unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
     if (pair_rows) {
-      // split == 6: two lanes per boundary row (even / odd slots), one shuffle merge
-      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
+      // two lanes per boundary row (even / odd slots), one shuffle merge
       if ((brow & ~31) < 2 * nbnd) {
         const int node = brow >> 1, half = brow & 1;
         double sv[B + 1];
@@ -912,7 +838,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         }
       }
     } else {
-      unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
       for (int base = 0; base < nbnd; base += cthreads) {
         if (base + (brow & ~31) >= nbnd) break;  // warp-uniform: no row for this warp
         const int node = base + brow;
@@ -921,23 +846,17 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           const int2 sw2 = slc[(p >> 5) - s_lo];
           const int lb = sw2.x + (p & 31);
           const int w = sw2.y;
-          const bool split = split_mode && base == 0;
-          const int j0 = split ? w - nh_s[node] : 0;
           double sv[B + 1];
 #pragma unroll
-          for (int i = 0; i <= B; ++i) sv[i] = split ? pv[i] : CUDART_INF;
+          for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
           const double lv = lam[lp];
-          if (a.trace && tid == 0 && base == 0) {
-            s_dummy = j0 + (int)__double2hiint(lv);
-            ck1 = clock64();
-          }
-          for (int jj = j0; jj < w; jj += 4) {
+          for (int jj = 0; jj < w; jj += 4) {
             int li[4];
             double cs[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const bool ok = jj + u < w;
-              const int idx = lb + 32 * (ok ? jj + u : j0);
+              const int idx = lb + 32 * (ok ? jj + u : 0);
               li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
               cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
               if (!ok) {
@@ -951,11 +870,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
             for (int u = 0; u < 4; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lu[u]));
           }
-          if (tid == 0 && base == 0) {
-            s_dummy = (int)__double2hiint(sv[B]);
-            ck2 = clock64();
-            F2M_TRACE16(s, 8);
-          }
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
           if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
@@ -963,67 +877,51 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
           mx = mx < ad ? ad : mx;
-          if (a.trace && s >= a.trace_first && s < a.trace_first + a.trace_count)
-            atomicMax(a.trace + ((((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4) + 7),
-                      globaltimer_ns());
-          if (tid == 0 && base == 0) ck3 = clock64();
         }
       }
     }
-    };
-    if (boundary_first) {
-      // the halo of sweep s was published early in the neighbours' sweep s-1 (they too start
-      // with their boundary rows), so it is normally staged already: publish first, then the
-      // interior rows overlap the neighbours' next exchange
-      halo_and_boundary_rows();
-      interior_rows();
-      if (warp == 0 && lane == 0) F2M_TRACE16(s, 4);
-    } else {
-      interior_rows();
-      if (warp == 0 && lane == 0) F2M_TRACE16(s, 4);
-    // boundary rows, first pass (RES): the own-CTA part of the row while the halo is in flight
-    // (slots are stored own-first, halo-last); the top-(B+1) multiset does not depend on order
-    if (split_mode && brow < nbnd) {
-      const int lp = bstart + brow, p = p0 + lp;
-      const int2 sw2 = slc[(p >> 5) - s_lo];
-      const int lb = sw2.x + (p & 31);
-      const int jo = sw2.y - nh_s[brow];
+    // interior slices: one thread per node (throughput-bound phase)
+    for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
+      const int p = sl * 32 + lane;
+      if (p >= a.n) continue;
+      const int lp = p - p0;
+      const int2 sw2 = slc[sl - s_lo];
+      const int lb = sw2.x + lane;
+      const int w = sw2.y;
       const double lv = lam[lp];
-      for (int jj = 0; jj < jo; jj += 4) {
-        int li[4];
-        double cs[4];
+      double sv[B + 1];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool ok = jj + u < jo;
-          const int idx = lb + 32 * (ok ? jj + u : 0);
-          li[u] = lid_s[idx];
-          cs[u] = cst_s[idx];
-          if (!ok) {
-            li[u] = lp;
-            cs[u] = CUDART_INF;
-          }
+      for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
+      int j = 0;
+      for (; j + 8 <= w; j += 8) {
+        int li[8];
+        double cs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = lb + 32 * (j + u);
+          li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
+          cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
         }
-        double lu[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) lu[u] = lam[li[u]];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) topk_bubble<B>(pv, dsub(dsub(cs[u], lv), lu[u]));
+        for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
       }
-    }
-      halo_and_boundary_rows();
-    }
-    if (a.trace && tid == 0 && s >= a.trace_first && s < a.trace_first + a.trace_count) {
-      unsigned long long* tr = a.trace + (((size_t)(s - a.trace_first) * (G + 1) + blockIdx.x) << 4);
-      tr[12] = ck1 - ck0;
-      tr[13] = ck2 - ck1;
-      tr[14] = ck3 - ck2;
-      tr[15] = clock64() - ck0;
+      for (; j < w; ++j) {
+        const int idx = lb + 32 * j;
+        const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
+        const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
+        topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
+      }
+      const double d = delta_of<B>(sv, a.update);
+      const double nl = dadd(lv, dmul(a.eta, d));
+      gout[p] = nl;
+      if (RES) lam_next[lp] = nl;
+      const double ad = fabs(d);
+      mx = mx < ad ? ad : mx;
     }
     {
       const unsigned long long wm = warp_max_nonneg(mx);
       if (lane == 0) red[s & 1][warp] = __longlong_as_double((long long)wm);
     }
-    if (tid == 0) F2M_TRACE16(s, 10);
     if (warp == 0 && lane == 0) {
       // stop decision for sweep s+1 (it overwrites glam[(s+2)%8]): verdict s-7 must be in
       unsigned long long w = s_word;
@@ -1047,16 +945,13 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       }
       s_word = w;
       s_stop[s & 1] = (w >> 32) ? (int)(w >> 32) - 1 : -1;
-      F2M_TRACE16(s, 11);
     }
     named_sync(2, cthreads);  // [B]
-    if (tid == 0) F2M_TRACE16(s, 5);
     if (warp == ncw - 1) {  // the CTA max goes out from the warp with the least boundary work
       const unsigned long long bm = warp_max_nonneg(lane < ncw ? red[s & 1][lane] : 0.0);
       if (lane == 0) {
         publish_cmax(a, ((size_t)(s % kCmaxRing) * G + c) * 2, __longlong_as_double((long long)bm), (unsigned)s + 1);
         s_done = s + 1;
-        F2M_TRACE16(s, 6);
       }
     }
     if (s_stop[s & 1] >= 0) break;
@@ -1071,6 +966,9 @@ static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t 
   void* args[] = {(void*)&a, (void*)&ctl};
   F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
 }
+
+constexpr int kResidentThreads = 768;
+constexpr int kStreamingThreads = 1024;
 
 // Resident (smem) layout: 768 threads per CTA (22 compute warps + 2 sync warps, 80 registers) with
 // the boundary-first sweep order: at 100k 3.18 us/sweep vs 3.40 (640), 3.48 (832), 3.73 (704),
@@ -1262,7 +1160,6 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.ll = ll.get();
     a.nb = nb;
     a.sdest = t.sdest.get();
-    a.row_nhalo = t.row_nhalo.get();
     a.poll_ns = 64;
     a.runahead = 1;
     DBuf<double> mean_out(1, s);
@@ -1274,10 +1171,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     // boundary rows first, only their warps meet at the halo hand-off; on small graphs (<= 256
     // rows per CTA: the boundary chain dominates, lanes are idle) two lanes per boundary row.
     // Measured: 10k 2.51 -> 2.09 us/sweep with pairs; at 100k / 200k pairs cost 6 %.
-    a.split = t.n <= 256 * G ? 6 : 4;
-    if (const char* e = std::getenv("F2M_SPLIT")) a.split = std::atoi(e);
-    if (const char* e = std::getenv("F2M_RUNAHEAD")) a.runahead = std::atoi(e);
-    if (const char* e = std::getenv("F2M_POLL_NS")) a.poll_ns = (unsigned)std::max(0, std::atoi(e));
+    a.pair_rows = t.n <= 256 * G ? 1 : 0;
     a.cmax = cmax.get();
     a.eta = cfg.eta;
     a.update = cfg.update;
@@ -1285,40 +1179,23 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.max_sweeps = max_sweeps;
     a.record = d_record;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
-    a.trace = nullptr;
     a.cta_base = 0;
     a.g_total = G;
     a.npeers = 0;
     a.ll_peers = nullptr;
     a.cmax_peers = nullptr;
     a.ll_mask = nullptr;
-    a.trace_first = a.trace_count = 0;
-    DBuf<unsigned long long> trace;
-    if (const char* tr = std::getenv("F2M_SWEEP_TRACE")) {
-      std::sscanf(tr, "%d,%d", &a.trace_first, &a.trace_count);
-      if (a.trace_count > 0) {
-        trace.alloc((size_t)a.trace_count * (G + 1) * 16, s);
-        F2M_CUDA(cudaMemsetAsync(trace.get(), 0, trace.bytes(), s));
-        a.trace = trace.get();
-      }
-    }
     F2M_CUDA(cudaEventRecord(e0, s));
     {  // + 1 CTA: the convergence master
-      static int nt = -1;
-      if (nt < 0) {
-        const char* e = std::getenv("F2M_SWEEP_NT");
-        nt = e ? std::atoi(e) : 768;
-        if (nt != 512 && nt != 640 && nt != 1024) nt = 768;
-      }
-      g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg.b) + (t.resident ? ", resident, " : ", streaming, ") +
-                          std::to_string(t.resident ? nt : 1024) + "> (persistent: " + std::to_string(G) +
+      g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg.b) +
+                          (t.resident ? ", resident, " + std::to_string(kResidentThreads)
+                                      : ", streaming, " + std::to_string(kStreamingThreads)) +
+                          "> (persistent: " + std::to_string(G) +
                           " partition CTAs + 1 convergence-master CTA, LL halo exchange, " +
-                          std::to_string(t.smem_bytes) + " B smem/CTA)";
-      if (t.resident && nt == 512) dispatch_sweep5<true, 512>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
-      else if (t.resident && nt == 640) dispatch_sweep5<true, 640>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
-      else if (t.resident && nt == 768) dispatch_sweep5<true, 768>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
-      else if (t.resident) dispatch_sweep5<true, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
-      else dispatch_sweep5<false, 1024>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+                          std::to_string(t.smem_bytes) + " B smem/CTA" +
+                          (a.pair_rows ? ", two lanes per boundary row)" : ")");
+      if (t.resident) dispatch_sweep5<true, kResidentThreads>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+      else dispatch_sweep5<false, kStreamingThreads>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
       launched("gdp_sweep5");
     }
     F2M_CUDA(cudaEventRecord(e1, s));
@@ -1345,33 +1222,6 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
       F2M_CUDA(cudaMemcpyAsync(d_lam1, a.gl + (size_t)outbuf * a.gstride, sizeof(double) * t.n,
                                cudaMemcpyDeviceToDevice, s));
     outbuf = 1;
-    if (a.trace) {
-      F2M_CUDA(cudaStreamSynchronize(s));
-      std::vector<unsigned long long> hbuf(trace.n);
-      F2M_CUDA(cudaMemcpy(hbuf.data(), trace.get(), trace.bytes(), cudaMemcpyDeviceToHost));
-      if (FILE* f = std::fopen("f2m_sweep_trace.bin", "wb")) {
-        const int hdr[4] = {a.trace_first, a.trace_count, -(G + 1), 16};
-        std::fwrite(hdr, sizeof(int), 4, f);
-        std::fwrite(hbuf.data(), sizeof(unsigned long long), hbuf.size(), f);
-        std::vector<int32_t> noff(G + 1);
-        F2M_CUDA(cudaMemcpy(noff.data(), t.nbr_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
-        std::vector<int32_t> nbr(std::max(noff[G], 1));
-        F2M_CUDA(cudaMemcpy(nbr.data(), t.nbr.get(), sizeof(int32_t) * nbr.size(), cudaMemcpyDeviceToHost));
-        std::fwrite(noff.data(), sizeof(int32_t), noff.size(), f);
-        std::fwrite(nbr.data(), sizeof(int32_t), noff[G], f);
-        // per-CTA partition facts: cta_lo[G+1], cta_int_hi[G], cta_nint[G], halo_off[G+1]
-        std::vector<int32_t> tmp(G + 1);
-        F2M_CUDA(cudaMemcpy(tmp.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
-        std::fwrite(tmp.data(), sizeof(int32_t), G + 1, f);
-        F2M_CUDA(cudaMemcpy(tmp.data(), t.cta_int_hi.get(), sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-        std::fwrite(tmp.data(), sizeof(int32_t), G, f);
-        F2M_CUDA(cudaMemcpy(tmp.data(), t.cta_nint.get(), sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-        std::fwrite(tmp.data(), sizeof(int32_t), G, f);
-        F2M_CUDA(cudaMemcpy(tmp.data(), t.halo_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost));
-        std::fwrite(tmp.data(), sizeof(int32_t), G + 1, f);
-        std::fclose(f);
-      }
-    }
   }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -1609,6 +1459,7 @@ void validate_engine(const f2m_engine_config& c) {
   if (!(c.eta > 0.0) || c.eta > 1.0) throw Error(F2M_E_ARGUMENT, "EngineConfig: eta must be in (0, 1]");
   if (!(c.eps > 0.0)) throw Error(F2M_E_ARGUMENT, "EngineConfig: eps must be > 0");
   if (c.max_sweeps < 0) throw Error(F2M_E_ARGUMENT, "EngineConfig: max_sweeps must be >= 0");
+  if (c.num_gpus < 0 || c.num_gpus > 32) throw Error(F2M_E_ARGUMENT, "EngineConfig: num_gpus must be in [0, 32]");
 }
 
 static void check_degree(const f2m_graph& g, int b) {
@@ -1986,7 +1837,6 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.ll = d_ll;
     a.nb = std::max(t.nboundary, 1);
     a.sdest = t.sdest.get();
-    a.row_nhalo = t.row_nhalo.get();
     a.poll_ns = 64;
     a.runahead = 1;
     a.defer_eps = 0.0;
@@ -1994,7 +1844,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.m = t.m;
     a.approx_sum = g->approx_sum.get();
     a.mean_out = nullptr;
-    a.split = t.n <= 256 * G ? 6 : 4;
+    a.pair_rows = t.n <= 256 * G ? 1 : 0;
     a.cmax = d_cmax;
     a.eta = cfg->eta;
     a.update = cfg->update;
@@ -2002,8 +1852,6 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.max_sweeps = max_sweeps;
     a.record = nullptr;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
-    a.trace = nullptr;
-    a.trace_first = a.trace_count = 0;
     a.cta_base = rank * Gp;
     a.g_total = G;
     a.npeers = world;
@@ -2017,11 +1865,13 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
       launched("ll_mask");
     }
     a.ll_mask = mask.get();  // freed (stream-ordered) after the sweep kernel
-    g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg->b) + (t.resident ? ", resident, 768" : ", streaming, 1024") +
+    g_last_sweep_desc = "k_gdp_sweep5<b=" + std::to_string(cfg->b) +
+                        (t.resident ? ", resident, " + std::to_string(kResidentThreads)
+                                    : ", streaming, " + std::to_string(kStreamingThreads)) +
                         "> multi-rank (rank " + std::to_string(rank) + "/" + std::to_string(world) + ": " +
                         std::to_string(Gp) + " of " + std::to_string(G) + " partition CTAs + 1 master, LL rings in every rank's memory)";
-    if (t.resident) dispatch_sweep5<true, 768>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
-    else dispatch_sweep5<false, 1024>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
+    if (t.resident) dispatch_sweep5<true, kResidentThreads>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
+    else dispatch_sweep5<false, kStreamingThreads>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
     launched("gdp_sweep5_multi");
   });
 }

@@ -143,8 +143,6 @@ struct Topology {
   DBuf<int32_t> halo_off;      // [ctas+1]
   DBuf<int32_t> halo;          // positions (sorted per CTA)
   DBuf<uint16_t> slidx;        // [sell_slots]
-  DBuf<int32_t> nbr_off;       // [ctas+1] CTA adjacency (owners of halo nodes; trace tooling)
-  DBuf<int32_t> nbr;
   // LL halo exchange: CTA c's boundary nodes are positions [p0_c + nint_c, p1_c);
   // boundary node p publishes its multiplier at LL index boff[c] + (p - p0_c - nint_c).
   DBuf<int32_t> cta_nint;      // [ctas] interior node count

@@ -133,12 +133,15 @@ def test_c_abi_host_only_calls():
     class Cfg(ctypes.Structure):
         _fields_ = [("b", ctypes.c_int), ("eta", ctypes.c_double), ("eps", ctypes.c_double),
                     ("max_sweeps", ctypes.c_int), ("mode", ctypes.c_int), ("update", ctypes.c_int),
-                    ("init", ctypes.c_int), ("threads", ctypes.c_int)]
+                    ("init", ctypes.c_int), ("threads", ctypes.c_int), ("num_gpus", ctypes.c_int)]
     lib.f2m_last_error.restype = ctypes.c_char_p
     assert lib.f2m_engine_config_validate(ctypes.byref(Cfg(2, 0.5, 1e-9, 100, 0, 0, 0, 0))) == 0
     assert lib.f2m_engine_config_validate(ctypes.byref(Cfg(2, 0.0, 1e-9, 100, 0, 0, 0, 0))) == 1
     assert b"eta" in lib.f2m_last_error()
     assert lib.f2m_engine_config_validate(ctypes.byref(Cfg(9, 0.5, 1e-9, 100, 0, 0, 0, 0))) == 1
+    assert lib.f2m_engine_config_validate(ctypes.byref(Cfg(2, 0.5, 1e-9, 100, 0, 0, 0, 0, 8))) == 0
+    assert lib.f2m_engine_config_validate(ctypes.byref(Cfg(2, 0.5, 1e-9, 100, 0, 0, 0, 0, -1))) == 1
+    assert b"num_gpus" in lib.f2m_last_error()
 
 
 def test_oracle_vs_live_reference_small(orc, ref):
