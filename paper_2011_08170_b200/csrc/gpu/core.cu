@@ -45,7 +45,7 @@ const cudaDeviceProp& device_props(int dev) {
 Topology::~Topology() {
   if (stream) {
     cudaSetDevice(dev);
-    eu.release(); ev.release(); perm.release(); iperm.release(); deg.release();
+    eu.release(); ev.release(); perm.release(); iperm.release(); perm0.release(); iperm0.release(); deg.release();
     sptr.release(); swidth.release(); scol.release(); seid.release(); cta_lo.release();
     halo_off.release(); halo.release(); slidx.release();
     cta_int_hi.release(); cta_nint.release(); boff.release(); halo_pub.release();
@@ -364,6 +364,7 @@ __global__ void k_local_sizes(int ctas, int n, const int32_t* __restrict__ lo, c
   int p0, p1;
   own_range(c, n, lo, p0, p1);
   atomicMax(max_local, (p1 - p0) + (hoff[c + 1] - hoff[c]));
+  atomicMax(max_local + 1, hoff[c + 1] - hoff[c]);  // halo entries alone
   atomicMax(max_slots, (unsigned long long)(sptr[lo[c + 1]] - sptr[lo[c]]));
 }
 
@@ -540,18 +541,19 @@ static void build_local_index(Topology& t) {
   }
   // sizes
   {
-    DBuf<int> ml(1, s);
+    DBuf<int> ml(2, s);
     DBuf<unsigned long long> ms(1, s);
-    F2M_CUDA(cudaMemsetAsync(ml.get(), 0, sizeof(int), s));
+    F2M_CUDA(cudaMemsetAsync(ml.get(), 0, 2 * sizeof(int), s));
     F2M_CUDA(cudaMemsetAsync(ms.get(), 0, sizeof(unsigned long long), s));
     k_local_sizes<<<grid_for(G, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.halo_off.get(), t.sptr.get(), ml.get(),
                                                    ms.get());
     launched("local_sizes");
     int64_t* hs = pinned_scratch();  // both sizes with one synchronisation
-    F2M_CUDA(cudaMemcpyAsync(hs + 1, ml.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 1, ml.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaMemcpyAsync(hs + 2, ms.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
-    t.max_local = *reinterpret_cast<const int*>(hs + 1);
+    t.max_local = reinterpret_cast<const int*>(hs + 1)[0];
+    t.max_halo = reinterpret_cast<const int*>(hs + 1)[1];
     t.max_cta_slots = hs[2];
   }
   const size_t limit = sweep_smem_limit(t.dev);
@@ -591,9 +593,9 @@ static void build_local_index(Topology& t) {
       launched("halo_pub");
     }
   }
-  // [lam regions][halo ids (<= max_local ints)][resident: cost + local index per slot]
+  // [lam regions][halo LL ids (max halo ints, 16-byte aligned)][resident: cost + local index per slot]
   const size_t lam_aligned = (lam_bytes + 15) & ~size_t(15);
-  const size_t ids_bytes = (size_t)(lam_aligned / sizeof(double)) * sizeof(int);
+  const size_t ids_bytes = (((size_t)t.max_halo * sizeof(int)) + 15) & ~size_t(15);
   // boundary count and the per-CTA slice table size (v5: (slot offset, width) per slice, 16-byte
   // aligned) from one stream synchronisation
   int max_slices = 0;
@@ -606,7 +608,7 @@ static void build_local_index(Topology& t) {
     t.nboundary = hs[0];
     for (int c = 0; c < G; ++c) max_slices = std::max(max_slices, lo[c + 1] - lo[c]);
   }
-  const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int2) + (size_t)max_slices * 32;  // + row halo counts
+  const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int2);
   const size_t resident_bytes = 2 * lam_aligned + ids_bytes +
                                 (size_t)t.max_cta_slots * (sizeof(double) + sizeof(uint16_t)) + slice_bytes;
   const size_t streaming_bytes = lam_aligned + ids_bytes + slice_bytes;
@@ -632,6 +634,14 @@ void finalize_topology(Topology& t) {
   if (m > 0) {
     k_degrees<<<grid_for(m, 256), 256, 0, s>>>(m, t.eu.get(), t.ev.get(), t.perm.get(), t.deg.get());
     launched("degrees");
+  }
+  // keep the spatial order itself: a re-partitioned replica (multi.cu) starts from it, not from
+  // the CTA-local order below (which is only coherent at this partition's granularity)
+  t.perm0.alloc(n, s);
+  t.iperm0.alloc(n, s);
+  if (n > 0) {
+    F2M_CUDA(cudaMemcpyAsync(t.perm0.get(), t.perm.get(), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+    F2M_CUDA(cudaMemcpyAsync(t.iperm0.get(), t.iperm.get(), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
   }
   // CTA partition (contiguous slice ranges balanced by degree + a per-slice constant), then
   // a CTA-local order: interior nodes first, boundary nodes last, each by descending degree

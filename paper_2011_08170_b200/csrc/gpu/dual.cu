@@ -386,10 +386,12 @@ struct Sweep4Args {
   int max_sweeps;
   double* record;
   int lam_stride;
+  int halo_stride;           // ints of the halo LL-id region (max halo, multiple of 4)
   const int32_t* __restrict__ sdest;     // v5: slot -> halo-last slot
   unsigned poll_ns;          // v5: sync-warp back-off between unproductive halo polls
   int runahead;              // v5: stage the next sweep's halo while this sweep computes
-  int pair_rows;             // two lanes per boundary row (small graphs: <= 256 rows per CTA)
+  int pair_rows;             // two lanes per boundary row (small graphs: <= 256 rows per CTA); selects
+                             // the PAIR instantiation
   // deferred threshold (v5): defer_eps > 0 -> threshold = defer_eps * mean_cost, where the master
   // CTA computes mean_cost (sequential sum of cost[0..m) / m, graph.cpp:47-49) during the solve
   double defer_eps;
@@ -630,7 +632,7 @@ __device__ __forceinline__ void publish_cmax(const Sweep4Args& a, size_t off, do
   for (int q = 0; q < a.npeers; ++q) st_ll_sys(a.cmax_peers[q] + off, v, tag);
 }
 
-template <int B, bool RES, int NT>
+template <int B, bool RES, int NT, bool PAIR>
 __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[2][NT / 32];
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // others go straight to their interior rows. Two lanes per boundary row when the CTA has few of
   // them (small graphs: at 10k the boundary chain dominates and idle lanes are plentiful; at 100k+
   // the interior rows need the lanes)
-  const bool pair_rows = RES && a.pair_rows && 2 * nbnd <= cthreads;
+  const bool pair_rows = RES && PAIR && 2 * nbnd <= cthreads;
   const int bthreads = pair_rows ? 2 * nbnd : nbnd;  // threads (in rotated order) with boundary work
   const bool own_bar = bthreads <= cthreads;
   const int halo_bar = own_bar ? 64 + 32 * ((bthreads + 31) / 32) : cthreads + 64;
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   double* regA = reinterpret_cast<double*>(smem);
   double* regB = regA + (RES ? a.lam_stride : 0);
   int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
-  double* cst_s = reinterpret_cast<double*>(halo_s + a.lam_stride);
+  double* cst_s = reinterpret_cast<double*>(halo_s + a.halo_stride);
   uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
   // per-slice (slot offset, width) of this CTA: no global loads on the sweep path
   int2* slc = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(lid_s + (RES ? nslots : 0)) + 15) & ~uintptr_t(15));
@@ -959,34 +961,45 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   if (tid == 0) s_exit = 1;
 }
 
-template <int B, bool RES, int NT>
+template <int B, bool RES, int NT, bool PAIR>
 static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
-  auto fn = k_gdp_sweep5<B, RES, NT>;
+  auto fn = k_gdp_sweep5<B, RES, NT, PAIR>;
   F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&a, (void*)&ctl};
   F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
 }
 
+#ifndef F2M_STREAMING_THREADS
+#define F2M_STREAMING_THREADS 1024
+#endif
 constexpr int kResidentThreads = 768;
-constexpr int kStreamingThreads = 1024;
+constexpr int kStreamingThreads = F2M_STREAMING_THREADS;
 
 // Resident (smem) layout: 768 threads per CTA (22 compute warps + 2 sync warps, 80 registers) with
 // the boundary-first sweep order: at 100k 3.18 us/sweep vs 3.40 (640), 3.48 (832), 3.73 (704),
 // 3.66 (1024) — more warps hide more latency until ptxas' register budget (65536 / threads)
 // serialises each row's load chain (640 was best with the interior-first order). The streaming
 // layout keeps 1024 threads for memory-level parallelism.
-template <bool RES, int NT>
-static void dispatch_sweep5(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
+template <bool RES, int NT, bool PAIR>
+static void dispatch_sweep5_b(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
   switch (b) {
-    case 1: launch_sweep5<1, RES, NT>(a, ctl, ctas, smem, s); break;
-    case 2: launch_sweep5<2, RES, NT>(a, ctl, ctas, smem, s); break;
-    case 3: launch_sweep5<3, RES, NT>(a, ctl, ctas, smem, s); break;
-    case 4: launch_sweep5<4, RES, NT>(a, ctl, ctas, smem, s); break;
-    case 5: launch_sweep5<5, RES, NT>(a, ctl, ctas, smem, s); break;
-    case 6: launch_sweep5<6, RES, NT>(a, ctl, ctas, smem, s); break;
-    case 7: launch_sweep5<7, RES, NT>(a, ctl, ctas, smem, s); break;
-    default: launch_sweep5<8, RES, NT>(a, ctl, ctas, smem, s); break;
+    case 1: launch_sweep5<1, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 2: launch_sweep5<2, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 3: launch_sweep5<3, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 4: launch_sweep5<4, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 5: launch_sweep5<5, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 6: launch_sweep5<6, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 7: launch_sweep5<7, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    default: launch_sweep5<8, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
   }
+}
+
+// the three product forms: resident with two lanes per boundary row (small graphs), resident with
+// one thread per boundary row, streaming (slots read from global memory every sweep)
+static void dispatch_sweep5(const Topology& t, int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, cudaStream_t s) {
+  if (t.resident && a.pair_rows) dispatch_sweep5_b<true, kResidentThreads, true>(b, a, ctl, ctas, t.smem_bytes, s);
+  else if (t.resident) dispatch_sweep5_b<true, kResidentThreads, false>(b, a, ctl, ctas, t.smem_bytes, s);
+  else dispatch_sweep5_b<false, kStreamingThreads, false>(b, a, ctl, ctas, t.smem_bytes, s);
 }
 
 size_t sweep_smem_limit(int dev) {
@@ -1179,6 +1192,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.max_sweeps = max_sweeps;
     a.record = d_record;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.halo_stride = (t.max_halo + 3) & ~3;
     a.cta_base = 0;
     a.g_total = G;
     a.npeers = 0;
@@ -1194,8 +1208,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
                           " partition CTAs + 1 convergence-master CTA, LL halo exchange, " +
                           std::to_string(t.smem_bytes) + " B smem/CTA" +
                           (a.pair_rows ? ", two lanes per boundary row)" : ")");
-      if (t.resident) dispatch_sweep5<true, kResidentThreads>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
-      else dispatch_sweep5<false, kStreamingThreads>(cfg.b, a, ctl.get(), G + 1, t.smem_bytes, s);
+      dispatch_sweep5(t, cfg.b, a, ctl.get(), G + 1, s);
       launched("gdp_sweep5");
     }
     F2M_CUDA(cudaEventRecord(e1, s));
@@ -1852,6 +1865,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.max_sweeps = max_sweeps;
     a.record = nullptr;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.halo_stride = (t.max_halo + 3) & ~3;
     a.cta_base = rank * Gp;
     a.g_total = G;
     a.npeers = world;
@@ -1870,8 +1884,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
                                     : ", streaming, " + std::to_string(kStreamingThreads)) +
                         "> multi-rank (rank " + std::to_string(rank) + "/" + std::to_string(world) + ": " +
                         std::to_string(Gp) + " of " + std::to_string(G) + " partition CTAs + 1 master, LL rings in every rank's memory)";
-    if (t.resident) dispatch_sweep5<true, kResidentThreads>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
-    else dispatch_sweep5<false, kStreamingThreads>(cfg->b, a, ctl, Gp + 1, t.smem_bytes, s);
+    dispatch_sweep5(t, cfg->b, a, ctl, Gp + 1, s);
     launched("gdp_sweep5_multi");
   });
 }

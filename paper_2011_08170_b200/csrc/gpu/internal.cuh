@@ -121,6 +121,7 @@ struct Topology {
   int64_t m = 0;
   DBuf<int32_t> eu, ev;        // [m] sorted (u, v), u <= v (self-loops kept)
   DBuf<int32_t> perm, iperm;   // [n]
+  DBuf<int32_t> perm0, iperm0; // [n] the spatial order before the CTA-local reorder (re-partitioning)
   DBuf<int32_t> deg;           // [n] by position
   int64_t nslices = 0;
   int64_t sell_slots = 0;
@@ -155,6 +156,7 @@ struct Topology {
   DBuf<int32_t> sdest;         // [sell_slots] slot index in the halo-last order
   DBuf<uint8_t> row_nhalo;     // [n] halo slots in the row of each position
   int max_local = 0;           // max over CTAs of own + halo
+  int max_halo = 0;            // max over CTAs of halo entries
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
   int partition_override = 0;  // > 0: partition CTA count for finalize_topology (multi-GPU replicas)

@@ -109,9 +109,9 @@ static f2m_graph* replicate(const f2m_graph& g, int dev, int partition) {
     F2M_CUDA(cudaMemcpyPeerAsync(r.ev.get(), dev, t.ev.get(), t.dev, t.ev.bytes(), s));
     F2M_CUDA(cudaMemcpyPeerAsync(h->cost.get(), dev, g.cost.get(), t.dev, g.cost.bytes(), s));
   }
-  if (t.n > 0) {
-    F2M_CUDA(cudaMemcpyPeerAsync(r.perm.get(), dev, t.perm.get(), t.dev, t.perm.bytes(), s));
-    F2M_CUDA(cudaMemcpyPeerAsync(r.iperm.get(), dev, t.iperm.get(), t.dev, t.iperm.bytes(), s));
+  if (t.n > 0) {  // the spatial (Morton) order, re-partitioned below
+    F2M_CUDA(cudaMemcpyPeerAsync(r.perm.get(), dev, t.perm0.get(), t.dev, t.perm0.bytes(), s));
+    F2M_CUDA(cudaMemcpyPeerAsync(r.iperm.get(), dev, t.iperm0.get(), t.dev, t.iperm0.bytes(), s));
   }
   finalize_topology(r);
   attach_costs(*h);
