@@ -468,6 +468,18 @@ def uniform_2m_leg(comm, dev, n=2_000_000):
                     "dual_value": rep["dual_value"], "us_per_sweep": 1e3 * ms / max(sw, 1),
                     "gdp_iterations_per_s": sw / (ms * 1e-3), "kernel": f2m.last_sweep_kernel_desc(),
                     "reference_cpu_s_per_sweep_1_thread": 1.631})
+        # HBM roofline of the streaming kernel (the honest HBM configuration): algorithmic bytes
+        # and the DRAM bytes ncu measured per sweep, over this run's per-sweep time
+        peak, peak_src = _peaks()
+        per_s = 1e-3 * ms / max(sw, 1)
+        alg = g.sweep_bytes()
+        prof = _summary().get("gdp_sweep_2m", {})
+        dram = (prof["dram_bytes_per_launch"] / prof["sweeps_per_launch"]) if prof.get("dram_bytes_per_launch") else None
+        out["roofline"] = {"bound": "hbm", "achieved": alg / per_s / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": alg / per_s / 1e9 / peak, "algorithmic_bytes_per_sweep": alg,
+                           "traffic": dram, "dram_achieved": (dram / per_s / 1e9) if dram else None,
+                           "dram_frac": (dram / per_s / 1e9 / peak) if dram else None, "peak_source": peak_src,
+                           "traffic_source": prof.get("source")}
         lam_ids = np.asarray(st.lam)
         graph = g
     else:
@@ -654,6 +666,25 @@ def run_gpu(args):
                 "kernel_ms": kern_ms, "us_per_sweep": 1e3 * kern_ms / sw, "peak_source": peak_src,
                 "share_of_step": (kern_ms * 1e-3) / t_step}
 
+    # the regime the 100k kernel is actually in (its slots live in shared memory, DRAM traffic is
+    # 0.4% of the algorithmic bytes): issue slots and shared-memory wavefronts per sweep from the
+    # committed ncu capture, over this run's measured per-sweep time
+    summ = _summary().get("gdp_sweep", {})
+    sm_count, sm_mhz = 148, (clocks.summary().get("sm_mhz") or 1965.0)
+    if summ.get("warp_inst_per_launch"):
+        per_sweep_s = kern_ms * 1e-3 / sw
+        inst = summ["warp_inst_per_launch"] / summ["sweeps_per_launch"]
+        wav = summ["smem_wavefronts_per_launch"] / summ["sweeps_per_launch"]
+        issue_peak = 4.0 * sm_count * sm_mhz * 1e6          # 4 schedulers x 1 warp-instruction / cycle
+        smem_peak = 1.0 * sm_count * sm_mhz * 1e6           # 1 shared-memory wavefront / cycle / SM
+        roofline["secondary"] = [
+            {"bound": "issue", "achieved": inst / per_sweep_s / 1e9, "peak": issue_peak / 1e9,
+             "unit": "G warp-instructions/s", "frac": inst / per_sweep_s / issue_peak,
+             "per_sweep": inst, "source": summ.get("source")},
+            {"bound": "smem", "achieved": wav / per_sweep_s / 1e9, "peak": smem_peak / 1e9,
+             "unit": "G shared-memory wavefronts/s", "frac": wav / per_sweep_s / smem_peak, "per_sweep": wav,
+             "bank_conflict_share": summ["smem_ld_bank_conflicts_per_launch"] / summ["smem_wavefronts_per_launch"],
+             "source": summ.get("source")}]
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,

@@ -449,6 +449,10 @@ __device__ __forceinline__ void topk_merge(double (&s)[B + 1], const double (&o)
 }
 
 constexpr unsigned kPollBackoffNs = 64;
+#ifndef F2M_POLL_NS
+#define F2M_POLL_NS 64
+#endif
+constexpr unsigned kPollNs = F2M_POLL_NS;  // sync-warp back-off between unproductive halo polls
 
 // Convergence master: a whole CTA on its own SM. Each round it reads the LL max |delta| of every
 // CTA for a window of kMasterWindow sweeps in one pass (one L2 round trip for all of them), then
@@ -1173,7 +1177,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.ll = ll.get();
     a.nb = nb;
     a.sdest = t.sdest.get();
-    a.poll_ns = 64;
+    a.poll_ns = kPollNs;
     a.runahead = 1;
     DBuf<double> mean_out(1, s);
     a.defer_eps = defer_eps;
@@ -1850,7 +1854,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.ll = d_ll;
     a.nb = std::max(t.nboundary, 1);
     a.sdest = t.sdest.get();
-    a.poll_ns = 64;
+    a.poll_ns = kPollNs;
     a.runahead = 1;
     a.defer_eps = 0.0;
     a.cost = g->cost.get();

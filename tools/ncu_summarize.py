@@ -20,7 +20,9 @@ WANT = {
     "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_throughput_pct",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "dram__bytes.sum.per_second": "dram_bytes_per_s",
+    "lts__t_sectors.sum": "l2_sectors",
     "sm__inst_issued.avg.pct_of_peak_sustained_active": "issue_active_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_active_pct",
@@ -56,19 +58,10 @@ def summarize(path):
                     val = float(v)
                 except ValueError:
                     continue
-                unit = units[hdr.index(k)] if k in hdr else ""
-                if unit == "Kbyte":
-                    val *= 1e3
-                elif unit == "Mbyte":
-                    val *= 1e6
-                elif unit == "Gbyte":
-                    val *= 1e9
-                elif unit == "usecond":
-                    val *= 1e3
-                elif unit == "msecond":
-                    val *= 1e6
-                elif unit == "KB":
-                    val *= 1024
+                unit = (units[hdr.index(k)] if k in hdr else "").split("/")[0]
+                val *= {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "byte": 1.0,
+                        "nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+                        "second": 1e9, "s": 1e9, "Tbyte": 1e12}.get(unit, 1.0)
                 res[name] = val
         break
     return res
