@@ -298,6 +298,20 @@ __global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairs
   }
 }
 
+// Debug build only (-DF2M_WARP_PROFILE, tools/build_variant.sh): per-warp cycle accounting of the
+// persistent sweep kernel — halo hand-off wait, boundary rows, interior rows, end-of-sweep barrier —
+// summed over the sweeps of a launch and read back with f2m_debug_warp_profile. The product build
+// compiles none of it.
+#ifdef F2M_WARP_PROFILE
+constexpr int kProfCtas = 160, kProfWarps = 32, kProfFields = 8;
+__device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
+#define F2M_PROF_T(var) const long long var = clock64()
+#define F2M_PROF_ADD(f, v) (prof[f] += (unsigned long long)(v))
+#else
+#define F2M_PROF_T(var)
+#define F2M_PROF_ADD(f, v)
+#endif
+
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -780,7 +794,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // was published early in the neighbours' sweep s-1 (they too start with their boundary rows),
   // so it is normally staged already; publish, then the interior rows overlap the neighbours'
   // next exchange.
+#ifdef F2M_WARP_PROFILE
+  unsigned long long prof[kProfFields] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   for (int s = 0;; ++s) {
+    F2M_PROF_T(t0);
     double* lam = (RES && (s & 1)) ? regB : regA;
     double* lam_next = (s & 1) ? regA : regB;
     const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
@@ -791,6 +809,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     }
     double mx = 0.0;
     if (in_halo_bar) named_sync(3 + (s & 1), halo_bar);  // halo of sweep s staged
+    F2M_PROF_T(t1);
+    F2M_PROF_ADD(0, t1 - t0);
     unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
     if (pair_rows) {
       // two lanes per boundary row (even / odd slots), one shuffle merge
@@ -856,25 +876,26 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
           for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
           const double lv = lam[lp];
-          for (int jj = 0; jj < w; jj += 4) {
-            int li[4];
-            double cs[4];
+          // the warp's 32 lanes are the 32 rows of one boundary slice (bstart is slice-aligned):
+          // one width, so the interior rows' 8-slot batches apply without predication
+          int j = 0;
+          for (; j + 8 <= w; j += 8) {
+            int li[8];
+            double cs[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const bool ok = jj + u < w;
-              const int idx = lb + 32 * (ok ? jj + u : 0);
+            for (int u = 0; u < 8; ++u) {
+              const int idx = lb + 32 * (j + u);
               li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
               cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
-              if (!ok) {
-                li[u] = lp;
-                cs[u] = CUDART_INF;
-              }
             }
-            double lu[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) lu[u] = lam[li[u]];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lu[u]));
+            for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+          }
+          for (; j < w; ++j) {
+            const int idx = lb + 32 * j;
+            const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
+            const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
+            topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
           }
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
@@ -886,6 +907,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         }
       }
     }
+    F2M_PROF_T(t2);
+    F2M_PROF_ADD(1, t2 - t1);
     // interior slices: one thread per node (throughput-bound phase)
     for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
       const int p = sl * 32 + lane;
@@ -924,6 +947,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       const double ad = fabs(d);
       mx = mx < ad ? ad : mx;
     }
+    F2M_PROF_T(t3);
+    F2M_PROF_ADD(2, t3 - t2);
     {
       const unsigned long long wm = warp_max_nonneg(mx);
       if (lane == 0) red[s & 1][warp] = __longlong_as_double((long long)wm);
@@ -953,6 +978,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       s_stop[s & 1] = (w >> 32) ? (int)(w >> 32) - 1 : -1;
     }
     named_sync(2, cthreads);  // [B]
+    F2M_PROF_T(t4);
+    F2M_PROF_ADD(3, t4 - t3);
+    F2M_PROF_ADD(4, 1);
     if (warp == ncw - 1) {  // the CTA max goes out from the warp with the least boundary work
       const unsigned long long bm = warp_max_nonneg(lane < ncw ? red[s & 1][lane] : 0.0);
       if (lane == 0) {
@@ -962,6 +990,17 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     }
     if (s_stop[s & 1] >= 0) break;
   }
+#ifdef F2M_WARP_PROFILE
+  if (lane == 0 && c < kProfCtas && warp < kProfWarps) {
+    // static work of this warp: interior slices and their slot columns, boundary rows (per sweep)
+    int isl = 0, icol = 0;
+    for (int sl = s_lo + warp; sl < s_int; sl += ncw) { ++isl; icol += slc[sl - s_lo].y; }
+    prof[5] = isl;
+    prof[6] = icol;
+    prof[7] = (brow & ~31) < bthreads ? 1 : 0;
+    for (int f = 0; f < kProfFields; ++f) g_wprof[c][warp][f] = prof[f];
+  }
+#endif
   if (tid == 0) s_exit = 1;
 }
 
@@ -973,6 +1012,10 @@ static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t 
   F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
 }
 
+#ifndef F2M_PAIR_ROWS_PER_CTA
+#define F2M_PAIR_ROWS_PER_CTA 256
+#endif
+constexpr int kPairRowsPerCta = F2M_PAIR_ROWS_PER_CTA;  // two lanes per boundary row up to this many rows per CTA
 #ifndef F2M_STREAMING_THREADS
 #define F2M_STREAMING_THREADS 1024
 #endif
@@ -1188,7 +1231,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     // boundary rows first, only their warps meet at the halo hand-off; on small graphs (<= 256
     // rows per CTA: the boundary chain dominates, lanes are idle) two lanes per boundary row.
     // Measured: 10k 2.51 -> 2.09 us/sweep with pairs; at 100k / 200k pairs cost 6 %.
-    a.pair_rows = t.n <= 256 * G ? 1 : 0;
+    a.pair_rows = t.n <= kPairRowsPerCta * G ? 1 : 0;
     a.cmax = cmax.get();
     a.eta = cfg.eta;
     a.update = cfg.update;
@@ -1730,6 +1773,22 @@ void note_sweep_kernel(double ms, int sweeps) {
 
 extern "C" const char* f2m_last_sweep_kernel_desc(void) { return g_last_sweep_desc.c_str(); }
 
+// debug builds only (-DF2M_WARP_PROFILE): the per-warp cycle accounting of the last sweep launch,
+// [160 CTAs][32 warps][8] = {halo wait, boundary rows, interior rows, end barrier, sweeps,
+// interior slices, interior slot columns, has boundary rows}
+extern "C" int f2m_debug_warp_profile(unsigned long long* out, size_t count) {
+  return guard([&] {
+#ifdef F2M_WARP_PROFILE
+    if (count < (size_t)kProfCtas * kProfWarps * kProfFields) throw Error(F2M_E_ARGUMENT, "warp profile: buffer too small");
+    F2M_CUDA(cudaMemcpyFromSymbol(out, g_wprof, sizeof(g_wprof)));
+#else
+    (void)out;
+    (void)count;
+    throw Error(F2M_E_ARGUMENT, "warp profile: not a -DF2M_WARP_PROFILE build");
+#endif
+  });
+}
+
 extern "C" int f2m_last_sweep_kernel_ms(double* ms, int* sweeps) {
   if (ms) *ms = g_last_sweep_ms;
   if (sweeps) *sweeps = g_last_sweep_count;
@@ -1861,7 +1920,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.m = t.m;
     a.approx_sum = g->approx_sum.get();
     a.mean_out = nullptr;
-    a.pair_rows = t.n <= 256 * G ? 1 : 0;
+    a.pair_rows = t.n <= kPairRowsPerCta * G ? 1 : 0;
     a.cmax = d_cmax;
     a.eta = cfg->eta;
     a.update = cfg->update;

@@ -479,6 +479,11 @@ PYBIND11_MODULE(_f2m, m) {
     f2m::check(f2m_generate_instance_device(n, seed, box, reinterpret_cast<double*>(d_xy),
                                             reinterpret_cast<void*>(stream)));
   }, py::arg("n"), py::arg("seed"), py::arg("box"), py::arg("d_xy"), py::arg("stream") = 0);
+  m.def("debug_warp_profile", []() {
+    py::array_t<unsigned long long> out({160, 32, 8});
+    f2m::check(f2m_debug_warp_profile(out.mutable_data(), static_cast<size_t>(out.size())));
+    return out;
+  });
   m.def("set_sweep_partition", [](int ctas) { f2m_set_sweep_partition(ctas); }, py::arg("ctas"));
   m.def("set_gpu_list", [](const std::vector<int>& devices) {
     f2m::check(f2m_set_gpu_list(devices.data(), static_cast<int>(devices.size())));
