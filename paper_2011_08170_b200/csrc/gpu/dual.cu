@@ -997,7 +997,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     for (int sl = s_lo + warp; sl < s_int; sl += ncw) { ++isl; icol += slc[sl - s_lo].y; }
     prof[5] = isl;
     prof[6] = icol;
-    prof[7] = (brow & ~31) < bthreads ? 1 : 0;
+    // width of this warp's boundary slice (0: no boundary rows)
+    prof[7] = (!pair_rows && (brow & ~31) < nbnd) ? slc[((p0 + bstart + (brow & ~31)) >> 5) - s_lo].y : 0;
     for (int f = 0; f < kProfFields; ++f) g_wprof[c][warp][f] = prof[f];
   }
 #endif
@@ -1775,7 +1776,7 @@ extern "C" const char* f2m_last_sweep_kernel_desc(void) { return g_last_sweep_de
 
 // debug builds only (-DF2M_WARP_PROFILE): the per-warp cycle accounting of the last sweep launch,
 // [160 CTAs][32 warps][8] = {halo wait, boundary rows, interior rows, end barrier, sweeps,
-// interior slices, interior slot columns, has boundary rows}
+// interior slices, interior slot columns, boundary slice width}
 extern "C" int f2m_debug_warp_profile(unsigned long long* out, size_t count) {
   return guard([&] {
 #ifdef F2M_WARP_PROFILE

@@ -35,9 +35,12 @@ out = {"n": args.n, "us_per_sweep": 1e3 * ms / sw, "sweeps": sw,
        "busy_max_warp_mean": float((per[..., 1] + per[..., 2]).max(1).mean()),
        "busy_mean_warp_mean": float((per[..., 1] + per[..., 2]).mean()),
        "interior_slices_per_warp": np.bincount(P[:, :nw, 5].astype(int).ravel()).tolist(),
-       "boundary_warps_per_cta": float(P[:, :nw, 7].sum(1).mean())}
+       "boundary_warps_per_cta": float((P[:, :nw, 7] > 0).sum(1).mean()),
+       "boundary_width_mean": float(P[:, :nw, 7][P[:, :nw, 7] > 0].mean()),
+       "interior_width_mean": float((P[:, :nw, 6].sum() / max(P[:, :nw, 5].sum(), 1)))}
 # the busiest warp of a typical CTA
 c = int(np.argsort(tot.max(1))[G // 2])
+# per-warp boundary slice width (boundary warps own one 32-row boundary slice each)
 out["cta_example"] = {"cta": c, "warps": [[round(float(x)) for x in per[c, w]] + [int(P[c, w, 5]), int(P[c, w, 6]), int(P[c, w, 7])]
                                          for w in range(nw)]}
 print(json.dumps(out))
