@@ -379,9 +379,9 @@ int f2m_last_sweep_kernel_ms(double* ms, int* sweeps);
  * arguments, grid shape). Valid until the next solve; never NULL. */
 const char* f2m_last_sweep_kernel_desc(void);
 /* Debug builds only (nvcc -DF2M_WARP_PROFILE): per-warp cycle accounting of the most recent
- * persistent sweep launch, [160][32][8] counters (halo wait, boundary rows, interior rows,
+ * persistent sweep launch, [160][32][12] counters (halo wait, boundary rows, interior rows,
  * end-of-sweep barrier, sweeps, interior slices, interior slot columns, boundary slice width).
- * The product build returns F2M_E_ARGUMENT. */
+   Fields 8-10: boundary-row setup, scan, finish + publish. The product build returns F2M_E_ARGUMENT. */
 int f2m_debug_warp_profile(unsigned long long* out, size_t count);
 /* Algorithmic bytes per sweep of this graph's GDP kernel:
  * 4(n+1) + 2m*(4+8) + 16n. */

@@ -697,8 +697,12 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
   double* cst_s = reinterpret_cast<double*>(halo_s + a.halo_stride);
   uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
-  // per-slice (slot offset, width) of this CTA: no global loads on the sweep path
-  int2* slc = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(lid_s + (RES ? nslots : 0)) + 15) & ~uintptr_t(15));
+  // per-slice (slot offset, width) of this CTA: no global loads on the sweep path. The 16-byte
+  // alignment is computed on the offset from `smem` so the compiler keeps the shared address space
+  // (a uintptr_t round trip turned these into generic LD.E loads)
+  const size_t slc_off =
+      ((size_t)(reinterpret_cast<unsigned char*>(lid_s + (RES ? nslots : 0)) - smem) + 15) & ~size_t(15);
+  int2* slc = reinterpret_cast<int2*>(smem + slc_off);
   const double* __restrict__ gcost = a.scost + slot0;
   const uint16_t* __restrict__ glid = a.slidx + slot0;
   for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];

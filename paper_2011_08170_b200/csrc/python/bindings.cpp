@@ -480,7 +480,7 @@ PYBIND11_MODULE(_f2m, m) {
                                             reinterpret_cast<void*>(stream)));
   }, py::arg("n"), py::arg("seed"), py::arg("box"), py::arg("d_xy"), py::arg("stream") = 0);
   m.def("debug_warp_profile", []() {
-    py::array_t<unsigned long long> out({160, 32, 8});
+    py::array_t<unsigned long long> out({160, 32, 12});
     f2m::check(f2m_debug_warp_profile(out.mutable_data(), static_cast<size_t>(out.size())));
     return out;
   });

@@ -41,6 +41,10 @@ out = {"n": args.n, "us_per_sweep": 1e3 * ms / sw, "sweeps": sw,
 # the busiest warp of a typical CTA
 c = int(np.argsort(tot.max(1))[G // 2])
 # per-warp boundary slice width (boundary warps own one 32-row boundary slice each)
-out["cta_example"] = {"cta": c, "warps": [[round(float(x)) for x in per[c, w]] + [int(P[c, w, 5]), int(P[c, w, 6]), int(P[c, w, 7])]
+sub = P[:, :nw, 8:11] / np.maximum(sweeps[..., None], 1)
+out["boundary_row_phases"] = {"setup": float(sub[..., 0][P[:, :nw, 7] > 0].mean()),
+                              "scan": float(sub[..., 1][P[:, :nw, 7] > 0].mean()),
+                              "finish_publish": float(sub[..., 2][P[:, :nw, 7] > 0].mean())}
+out["cta_example"] = {"cta": c, "warps": [[round(float(x)) for x in per[c, w]] + [int(P[c, w, 5]), int(P[c, w, 6]), int(P[c, w, 7])] + [round(float(x)) for x in sub[c, w]]
                                          for w in range(nw)]}
 print(json.dumps(out))
