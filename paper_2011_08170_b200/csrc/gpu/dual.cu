@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairs
 // summed over the sweeps of a launch and read back with f2m_debug_warp_profile. The product build
 // compiles none of it.
 #ifdef F2M_WARP_PROFILE
-constexpr int kProfCtas = 160, kProfWarps = 32, kProfFields = 8;
+constexpr int kProfCtas = 160, kProfWarps = 32, kProfFields = 12;
 __device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
 #define F2M_PROF_T(var) const long long var = clock64()
 #define F2M_PROF_ADD(f, v) (prof[f] += (unsigned long long)(v))
@@ -799,7 +799,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // so it is normally staged already; publish, then the interior rows overlap the neighbours'
   // next exchange.
 #ifdef F2M_WARP_PROFILE
-  unsigned long long prof[kProfFields] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof[kProfFields] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   for (int s = 0;; ++s) {
     F2M_PROF_T(t0);
@@ -880,6 +880,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
           for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
           const double lv = lam[lp];
+          F2M_PROF_T(ta);
           // the warp's 32 lanes are the 32 rows of one boundary slice (bstart is slice-aligned):
           // one width, so the interior rows' 8-slot batches apply without predication
           int j = 0;
@@ -901,6 +902,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
             const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
             topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
           }
+          F2M_PROF_T(tb);
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
           if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
@@ -908,6 +910,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
           mx = mx < ad ? ad : mx;
+          F2M_PROF_T(tc);
+          F2M_PROF_ADD(8, ta - t1);
+          F2M_PROF_ADD(9, tb - ta);
+          F2M_PROF_ADD(10, tc - tb);
         }
       }
     }
