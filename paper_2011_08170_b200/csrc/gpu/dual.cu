@@ -312,6 +312,13 @@ __device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
 #define F2M_PROF_ADD(f, v)
 #endif
 
+// Streaming form: one TMA bulk prefetch of a slice's slot arrays (costs, local indices) into L2,
+// issued a slice ahead by lane 0 of the warp that will scan it, so the scan's loads hit L2 while
+// HBM streams the next slice in the background.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -319,6 +326,10 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+#ifndef F2M_L2_PREFETCH_AHEAD
+#define F2M_L2_PREFETCH_AHEAD 1
+#endif
+constexpr int kPrefetchAhead = F2M_L2_PREFETCH_AHEAD;  // streaming form: slices of L2 prefetch per warp
 constexpr int kLamBufs = 8;     // convergence verdicts may lag the sweeps by up to 7
 constexpr int kCmaxRing = 64;   // CTAs stay within ~16 sweeps of every helper (see core.cu)
 
@@ -921,6 +932,14 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     F2M_PROF_ADD(1, t2 - t1);
     // interior slices: one thread per node (throughput-bound phase)
     for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
+      if (!RES && lane == 0) {
+        // this warp's slice F2M_L2_PREFETCH_AHEAD slices from now, or (near the end of the sweep)
+        // its first slice of the next sweep: the slot arrays are the same every sweep
+        const int nx = sl + kPrefetchAhead * ncw < s_int ? sl + kPrefetchAhead * ncw : s_lo + warp;
+        const int2 q = slc[nx - s_lo];
+        prefetch_l2(gcost + q.x, (unsigned)q.y * 32u * 8u);
+        prefetch_l2(glid + q.x, (unsigned)q.y * 32u * 2u);
+      }
       const int p = sl * 32 + lane;
       if (p >= a.n) continue;
       const int lp = p - p0;
