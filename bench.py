@@ -502,63 +502,54 @@ def uniform_2m_leg(comm, dev, n=2_000_000):
 
 
 def allpairs_leg(dev, sizes=((2000, 200), (8000, 30))):
-    """north_star's all-pairs scans: complete graphs (build_knn_graph with k >= n-1, graph.cpp:175)
-    whose sweeps recompute every distance from the points (k_allpairs_sweep). Fixed sweep counts;
-    the roofline is the FP64 pipe: fp64 instructions per launch (ncu, profiles/ncu_summary.json
-    allpairs_*) over the kernel time against the measured fp64 issue peak (tools/microbench/tput.cu)."""
+    """north_star's all-pairs scans: complete graphs (build_knn_graph with k >= n-1, graph.cpp:175).
+    Two bit-identical kernels, fixed sweep counts each:
+      dense      (default) streams an n x n distance matrix computed once per graph — bound by
+                 HBM (n = 8,000: 512 MB per sweep) or L2 (n = 2,000: 32 MB, cache-resident);
+      recompute  recomputes every distance from the points each sweep — bound by the FP64 pipe:
+                 fp64 thread-instructions per pair (ncu, profiles/ncu_summary.json allpairs_*) x
+                 pair evaluations/s against the measured FP64 issue peak (tools/microbench/tput.cu)."""
     import paper_2011_08170_b200 as f2m
     summ = _summary()
-    peak = summ.get("fp64_peak", {})
+    fp64_peak = summ.get("fp64_peak", {})
+    hbm_peak, hbm_src = _peaks()
     out = []
-    for n, sweeps in sizes:
-        g = f2m.build_knn_graph(f2m.generate_instance(n, SEED, 1000.0), n - 1)
-        st = f2m.make_initial_state(g)
-        f2m.jacobi_sweeps(g, st, 5)  # warm-up
-        st = f2m.make_initial_state(g)
-        f2m.jacobi_sweeps(g, st, sweeps)
-        ms, sw = f2m.last_sweep_kernel()
-        assert "allpairs" in f2m.last_sweep_kernel_desc()
-        pairs = n * (n - 1) * sw
-        row = {"n": n, "sweeps": sw, "kernel_ms": ms, "us_per_sweep": 1e3 * ms / sw,
-               "pair_evaluations_per_s": pairs / (ms * 1e-3), "kernel": f2m.last_sweep_kernel_desc()}
-        prof = summ.get(f"allpairs_{n}")
-        if prof and peak.get("fp64_inst_per_s"):
-            achieved = prof["fp64_thread_inst_per_pair"] * pairs / (ms * 1e-3)
-            row["roofline"] = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak["fp64_inst_per_s"] / 1e12,
-                               "unit": "T fp64 thread-instructions/s", "frac": achieved / peak["fp64_inst_per_s"],
-                               "fp64_pipe_active_ncu": prof.get("fp64_pipe_active_pct"),
-                               "source": prof.get("source"), "peak_source": peak.get("source")}
-        out.append(row)
+    try:
+        for n, sweeps in sizes:
+            g = f2m.build_knn_graph(f2m.generate_instance(n, SEED, 1000.0), n - 1)
+            row = {"n": n, "sweeps": sweeps}
+            for mode, name in ((2, "dense"), (1, "recompute")):
+                f2m._f2m.set_allpairs_mode(mode)
+                st = f2m.make_initial_state(g)
+                f2m.jacobi_sweeps(g, st, 5)  # warm-up (and the dense matrix, once per graph)
+                st = f2m.make_initial_state(g)
+                f2m.jacobi_sweeps(g, st, sweeps)
+                ms, sw = f2m.last_sweep_kernel()
+                desc = f2m.last_sweep_kernel_desc()
+                assert "allpairs" in desc
+                pairs = n * (n - 1) * sw
+                r = {"kernel_ms": ms, "us_per_sweep": 1e3 * ms / sw, "pair_evaluations_per_s": pairs / (ms * 1e-3),
+                     "kernel": desc}
+                if mode == 2:
+                    byts = 8.0 * n * n * sw
+                    r["roofline"] = {"bound": "hbm" if 8 * n * n > 126e6 else "l2 (matrix cache-resident)",
+                                     "achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                     "frac": byts / (ms * 1e-3) / 1e9 / hbm_peak,
+                                     "bytes_per_sweep": 8.0 * n * n, "peak_source": hbm_src}
+                prof = summ.get(f"allpairs_{n}")
+                if mode == 1 and prof and fp64_peak.get("fp64_inst_per_s"):
+                    achieved = prof["fp64_thread_inst_per_pair"] * pairs / (ms * 1e-3)
+                    r["roofline"] = {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak["fp64_inst_per_s"] / 1e12,
+                                     "unit": "T fp64 thread-instructions/s", "frac": achieved / fp64_peak["fp64_inst_per_s"],
+                                     "fp64_pipe_active_ncu": prof.get("fp64_pipe_active_pct"),
+                                     "source": prof.get("source"), "peak_source": fp64_peak.get("source")}
+                row[name] = r
+            row["speedup_dense_over_recompute"] = row["recompute"]["us_per_sweep"] / row["dense"]["us_per_sweep"]
+            out.append(row)
+            del g
+    finally:
+        f2m._f2m.set_allpairs_mode(2)
     return out
-
-
-def sharded_p2p_leg(g, comm, dev, sweeps=256):
-    """The same 2M sweeps through the fused peer-memory engine (one persistent kernel per rank,
-    halo and sweep maxima stored into the peers' memory; sharded.ShardedP2P)."""
-    import torch
-    import torch.distributed as dist
-
-    import paper_2011_08170_b200 as f2m
-    from paper_2011_08170_b200.sharded import ShardedP2P
-
-    sched = ShardedP2P(g, comm)
-    lam0 = torch.zeros(sched.stride * comm.world, dtype=torch.float64, device=dev)
-    f2m._f2m.initial_state_positions(g, lam0.data_ptr(), 2, "local-midpoint", torch.cuda.current_stream(dev).cuda_stream)
-    sched.run(lam0, -1.0, 8)  # warm-up
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sched.launch(lam0, -1.0, sweeps, e0, e1)
-    torch.cuda.synchronize()
-    lam_full, res = sched.collect()
-    assert res["sweeps"] == sweeps
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    per_us = float(ms.item()) * 1e3 / sweeps
-    return {"workload": f"same as sharded_2m, fused peer-memory engine x{comm.world}",
-            "ranks": comm.world, "us_per_sweep": per_us, "gdp_iterations_per_s": 1e6 / per_us,
-            "algorithmic_GBps": g.sweep_bytes() / (per_us * 1e-6) / 1e9,
-            "halo_values_per_sweep": sched.halo_values,
-            "kernel": f"k_p2p_solve<2> (one persistent launch per rank, {sched.ctas} CTAs x 1024; LL halo stores "
-                      f"into peer memory, per-sweep maxima boards, 2 grid barriers per sweep)"}
 
 
 def run_gpu(args):

@@ -360,6 +360,13 @@ int f2m_sweep_multi_result(const void* d_ctl, int* sweeps, int* converged, doubl
 int f2m_sweep_multi_traffic(const f2m_graph* g, int rank, int world, int64_t* remote_ll_stores,
                             int64_t* remote_max_stores);
 
+/* Complete graphs whose costs are the points' distances (build_knn_graph with k >= n-1,
+ * graph.cpp:175; n <= 8192) sweep with a dedicated kernel: mode 2 (default) streams an n x n
+ * distance matrix computed once per graph (n^2 doubles of device memory), 1 recomputes every cost
+ * from the points each sweep (no extra memory, FP64-bound), 0 uses the CSR kernels. All three are
+ * bit-identical. Process-wide; takes effect at the next solve. */
+int f2m_set_allpairs_mode(int mode);
+
 /* ---- single-process multi-GPU (f2m_engine_config.num_gpus > 1) ------------------------------
  * Devices of rank 0..num_gpus-1 (default: the graph's device and the next num_gpus-1, modulo the
  * device count). A device may repeat: those ranks then share its SMs (test configurations on one

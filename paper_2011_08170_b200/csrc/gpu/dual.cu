@@ -207,6 +207,16 @@ __device__ __forceinline__ unsigned long long warp_max_nonneg_ap(double x) {
   return ((unsigned long long)mhi << 32) | mlo;
 }
 
+// One TMA bulk prefetch of [p, p + bytes) into L2 (cp.async.bulk.prefetch.L2: 16-byte aligned
+// start and size, so the range is widened to 16-byte boundaries). The streaming sweep form issues
+// it a slice ahead per warp, the dense all-pairs form a row ahead.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  if (!bytes) return;
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo)) : "memory");
+}
+
 // ---------------------------------------------------------------- all-pairs Jacobi sweep
 // Complete graphs (build_knn_graph with k >= n-1, graph.cpp:175) whose costs are the points'
 // distances: every cost is recomputed on the fly as distance() does it (instance.cpp:126-141:
@@ -215,11 +225,19 @@ __device__ __forceinline__ unsigned long long warp_max_nonneg_ap(double x) {
 // multipliers sit in shared memory; one warp per node scans its n-1 partners (lane-strided) and
 // the lanes' top lists are merged with shuffles. Same sweep/convergence protocol as k_gdp_sweep.
 constexpr int kAllPairsThreads = 512;
+#ifndef F2M_DENSE_THREADS
+#define F2M_DENSE_THREADS 1024
+#endif
+constexpr int kDenseThreads = F2M_DENSE_THREADS;  // the streamed form wants memory-level parallelism
 constexpr int kAllPairsMaxN = 8192;
+// complete graphs with distance costs: 0 = the CSR kernels, 1 = recompute every cost from the
+// points each sweep (FP64-bound), 2 = stream a once-computed distance matrix (default)
+static std::atomic<int> g_allpairs_mode{2};
 
 struct AllPairsArgs {
   int n;
   const double2* __restrict__ pts;  // position order
+  const double* __restrict__ dense; // DENSE form: n x n distances in position order
   int rounded;
   double* lam0;
   double* lam1;
@@ -230,15 +248,33 @@ struct AllPairsArgs {
   double* record;
 };
 
-template <int B>
-__global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairsArgs a, SweepCtl* ctl) {
+// DENSE form: the n x n distance matrix is computed once per graph (k_dense_distances, the same
+// exact fp64 sequence) and every sweep streams row v (coalesced, L2-resident up to n ~ 3,900) instead
+// of recomputing the square roots — HBM / L2-bound instead of FP64-bound.
+// D[p][q] = distance(point p, point q) in position order, distance()'s exact sequence
+// (instance.cpp:126-141: sqrt(dx*dx + dy*dy) without FMA, rounded mode floor(d + 0.5)) with dx taken
+// from the row's point as the recompute form does; symmetric bit for bit.
+__global__ void k_dense_distances(int n, const double2* __restrict__ pts, int rounded, double* __restrict__ d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * n) return;
+  const int p = (int)(i / n), q = (int)(i - (int64_t)p * n);
+  const double2 pv = pts[p], pu = pts[q];
+  const double dx = dsub(pv.x, pu.x), dy = dsub(pv.y, pu.y);
+  double c = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+  if (rounded) c = floor(dadd(c, 0.5));
+  d[i] = c;
+}
+
+template <int B, bool DENSE>
+__global__ void __launch_bounds__(DENSE ? kDenseThreads : kAllPairsThreads, 1) k_allpairs_sweep(AllPairsArgs a, SweepCtl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[kAllPairsThreads / 32];
+  __shared__ double red[(DENSE ? kDenseThreads : kAllPairsThreads) / 32];
   __shared__ double s_gmax;
   double2* pts = reinterpret_cast<double2*>(smem);
-  double* lam = reinterpret_cast<double*>(pts + a.n);
+  double* lam = DENSE ? reinterpret_cast<double*>(smem) : reinterpret_cast<double*>(pts + a.n);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < a.n; i += blockDim.x) pts[i] = a.pts[i];
+  if (!DENSE)
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) pts[i] = a.pts[i];
   int sweep = 0;
   double gmax = INFINITY;
   bool converged = false;
@@ -249,18 +285,38 @@ __global__ void __launch_bounds__(kAllPairsThreads, 1) k_allpairs_sweep(AllPairs
     __syncthreads();
     double mx = 0.0;
     for (int v = blockIdx.x * nwarps + warp; v < a.n; v += gridDim.x * nwarps) {
-      const double2 pv = pts[v];
       const double lv = lam[v];
       double s[B + 1];
 #pragma unroll
       for (int i = 0; i <= B; ++i) s[i] = CUDART_INF;
-      for (int u = lane; u < a.n; u += 32) {
-        if (u == v) continue;
-        const double2 pu = pts[u];
-        const double dx = dsub(pv.x, pu.x), dy = dsub(pv.y, pu.y);
-        double c = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
-        if (a.rounded) c = floor(dadd(c, 0.5));
-        topk_insert<B>(s, dsub(dsub(c, lv), lam[u]));
+      if (DENSE) {
+        const double* __restrict__ row = a.dense + (size_t)v * a.n;
+        // the warp's next row into L2 (one TMA bulk prefetch) while this one streams
+        const int vn = v + gridDim.x * nwarps;
+        if (lane == 0 && vn < a.n) prefetch_l2(a.dense + (size_t)vn * a.n, (unsigned)a.n * 8u);
+        int u = lane;
+        for (; u + 224 < a.n; u += 256) {  // 8 coalesced row loads in flight per lane
+          double c[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) c[q] = __ldcg(row + u + 32 * q);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const double z = dsub(dsub(c[q], lv), lam[u + 32 * q]);
+            topk_bubble<B>(s, u + 32 * q != v ? z : CUDART_INF);
+          }
+        }
+        for (; u < a.n; u += 32)
+          if (u != v) topk_insert<B>(s, dsub(dsub(__ldcg(row + u), lv), lam[u]));
+      } else {
+        const double2 pv = pts[v];
+        for (int u = lane; u < a.n; u += 32) {
+          if (u == v) continue;
+          const double2 pu = pts[u];
+          const double dx = dsub(pv.x, pu.x), dy = dsub(pv.y, pu.y);
+          double c = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+          if (a.rounded) c = floor(dadd(c, 0.5));
+          topk_insert<B>(s, dsub(dsub(c, lv), lam[u]));
+        }
       }
       warp_topk_merge<B>(s);
       if (lane == 0) {
@@ -311,13 +367,6 @@ __device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
 #define F2M_PROF_T(var)
 #define F2M_PROF_ADD(f, v)
 #endif
-
-// Streaming form: one TMA bulk prefetch of a slice's slot arrays (costs, local indices) into L2,
-// issued a slice ahead by lane 0 of the warp that will scan it, so the scan's loads hit L2 while
-// HBM streams the next slice in the background.
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -1129,18 +1178,21 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
   F2M_CUDA(cudaEventCreate(&e1));
   int error = 0, sweeps = 0, converged = 0, outbuf = 0;
   double final_max = INFINITY;
-  static int allpairs_env = -1;  // F2M_ALLPAIRS=0 forces the CSR kernels for complete graphs
-  if (allpairs_env < 0) {
-    const char* e = std::getenv("F2M_ALLPAIRS");
-    allpairs_env = (e && e[0] == '0') ? 0 : 1;
-  }
-  if (g.allpairs && allpairs_env && t.n <= kAllPairsMaxN) {
+  const int ap_mode = g_allpairs_mode.load();
+  if (g.allpairs && ap_mode != 0 && t.n <= kAllPairsMaxN) {
     const double2* pts = g.pts_pos.get();
+    const bool dense = ap_mode == 2;
+    if (dense && !g.dense.get()) {  // once per graph (n^2 doubles: 537 MB at the 8,192 cap)
+      g.dense.alloc((size_t)t.n * t.n, s);
+      k_dense_distances<<<grid_for((int64_t)t.n * t.n, 256), 256, 0, s>>>(t.n, pts, g.rounded, g.dense.get());
+      launched("dense_distances");
+    }
     DBuf<SweepCtl> ctl(1, s);
     F2M_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(SweepCtl), s));
     AllPairsArgs ap;
     ap.n = t.n;
     ap.pts = pts;
+    ap.dense = dense ? g.dense.get() : nullptr;
     ap.rounded = g.rounded;
     ap.lam0 = d_lam0;
     ap.lam1 = d_lam1;
@@ -1149,26 +1201,30 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     ap.threshold = defer_eps > 0.0 ? defer_eps * graph_mean(g) : threshold;
     ap.max_sweeps = max_sweeps;
     ap.record = d_record;
-    const size_t smem = (size_t)t.n * (sizeof(double2) + sizeof(double));
-    const int ctas = std::min(sweep_grid_ctas(t.dev), std::max(1, (t.n + 15) / 16));
-    g_last_sweep_desc = "k_allpairs_sweep<b=" + std::to_string(cfg.b) + "> (" + std::to_string(ctas) +
-                        " CTAs x 512, costs recomputed from the points, " + std::to_string(smem) + " B smem/CTA)";
+    const size_t smem = (size_t)t.n * ((dense ? 0 : sizeof(double2)) + sizeof(double));
+    // one row per warp; the dense form spreads its rows over every SM (up to 32 warps each)
+    const int sms = sweep_grid_ctas(t.dev);
+    const int nt = dense ? std::min(kDenseThreads, std::max(64, 32 * ((t.n + sms - 1) / sms))) : kAllPairsThreads;
+    const int wpc = nt / 32;
+    const int ctas = std::min(sms, std::max(1, (t.n + wpc - 1) / wpc));
+    g_last_sweep_desc = "k_allpairs_sweep<b=" + std::to_string(cfg.b) + (dense ? ", dense" : ", recompute") +
+                        "> (" + std::to_string(ctas) + " CTAs x " + std::to_string(nt) + ", " +
+                        (dense ? "distance matrix streamed, " : "costs recomputed from the points, ") +
+                        std::to_string(smem) + " B smem/CTA)";
     F2M_CUDA(cudaEventRecord(e0, s));
     SweepCtl* ctlp = ctl.get();
     void* args[] = {(void*)&ap, (void*)&ctlp};
+    auto launch = [&](const void* fn) {
+      F2M_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      F2M_CUDA(cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(nt), args, smem, s));
+    };
     switch (cfg.b) {
-#define F2M_AP(BB)                                                                                          \
-  case BB: {                                                                                                \
-    auto fn = k_allpairs_sweep<BB>;                                                                         \
-    F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kAllPairsThreads), args, smem, s)); \
-  } break;
+#define F2M_AP(BB)                                                                                        \
+  case BB:                                                                                                \
+    launch(dense ? (const void*)k_allpairs_sweep<BB, true> : (const void*)k_allpairs_sweep<BB, false>);  \
+    break;
       F2M_AP(1) F2M_AP(2) F2M_AP(3) F2M_AP(4) F2M_AP(5) F2M_AP(6) F2M_AP(7)
-      default: {
-        auto fn = k_allpairs_sweep<8>;
-        F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kAllPairsThreads), args, smem, s));
-      } break;
+      default: launch(dense ? (const void*)k_allpairs_sweep<8, true> : (const void*)k_allpairs_sweep<8, false>); break;
 #undef F2M_AP
     }
     launched("allpairs_sweep");
@@ -1802,6 +1858,13 @@ void note_sweep_kernel(double ms, int sweeps) {
 }  // namespace f2mgpu
 
 extern "C" const char* f2m_last_sweep_kernel_desc(void) { return g_last_sweep_desc.c_str(); }
+
+extern "C" int f2m_set_allpairs_mode(int mode) {
+  return guard([&] {
+    if (mode < 0 || mode > 2) throw Error(F2M_E_ARGUMENT, "f2m_set_allpairs_mode: mode must be 0, 1 or 2");
+    g_allpairs_mode.store(mode);
+  });
+}
 
 // debug builds only (-DF2M_WARP_PROFILE): the per-warp cycle accounting of the last sweep launch,
 // [160 CTAs][32 warps][8] = {halo wait, boundary rows, interior rows, end barrier, sweeps,

@@ -181,6 +181,7 @@ struct f2m_graph {
   // graph.cpp:175): the sweeps can recompute every cost on the fly from the points instead of
   // streaming the n(n-1)/2-edge CSR (all-pairs mode). Points in position order.
   f2mgpu::DBuf<double2> pts_pos;
+  mutable f2mgpu::DBuf<double> dense;  // all-pairs DENSE form: n x n distances, built on first use
   int rounded = 0;
   bool allpairs = false;
   // num_gpus > 1 solves: the graph replicated onto every GPU (partitioned into world x Gp CTAs)

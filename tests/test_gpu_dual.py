@@ -305,20 +305,32 @@ def test_streaming_kernel_matches_grid_barrier_kernel():
 
 
 # ------------------------------------------------------------------ all-pairs (complete graphs)
+@pytest.fixture
+def allpairs_mode(f2m):
+    yield lambda mode: f2m._f2m.set_allpairs_mode(mode)
+    f2m._f2m.set_allpairs_mode(2)
+
+
+@pytest.mark.parametrize("mode", [2, 1, 0])
 @pytest.mark.parametrize("n,seed,rounded", [(8, 1, False), (60, 2, False), (300, 3, True), (1200, 4, False)])
-def test_allpairs_complete_graph_matches_oracle(f2m, n, seed, rounded):
-    """k >= n-1 builds the complete graph (graph.cpp:175); its sweeps recompute every cost from
-    the points (k_allpairs_sweep). lambda, sweep count, final max|delta|, dual value and the
-    per-sweep maxima must equal the C oracle's CSR solve bit for bit."""
+def test_allpairs_complete_graph_matches_oracle(f2m, allpairs_mode, n, seed, rounded, mode):
+    """k >= n-1 builds the complete graph (graph.cpp:175); its sweeps stream a once-computed
+    distance matrix (mode 2, the default), recompute every cost from the points (mode 1) or use
+    the CSR kernels (mode 0). lambda, sweep count, final max|delta|, dual value and the per-sweep
+    maxima must equal the C oracle's CSR solve bit for bit in every mode."""
     from oracle import oracle as orc
 
+    allpairs_mode(mode)
     inst = f2m.generate_instance(n, seed)
     if rounded:
         inst.mode = f2m.DistanceMode.EUC2D_ROUNDED
     g = f2m.build_knn_graph(inst, n - 1)
     assert g.m == n * (n - 1) // 2
     st, rep = f2m.solve_duals(g, max_sweeps=20000)
-    assert "allpairs" in f2m.last_sweep_kernel_desc()
+    desc = f2m.last_sweep_kernel_desc()
+    assert ("allpairs" in desc) == (mode != 0)
+    assert mode != 2 or "dense" in desc
+    assert mode != 1 or "recompute" in desc
     og = orc.build_knn_graph(inst.points_array(), n - 1, rounded=rounded)
     lam, orep = orc.solve_duals(og, max_sweeps=20000)
     assert rep["sweeps"] == orep["sweeps"] and rep["converged"] == orep["converged"]
