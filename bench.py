@@ -482,6 +482,24 @@ def uniform_2m_leg(comm, dev, n=2_000_000):
                            "traffic_source": prof.get("source")}
         lam_ids = np.asarray(st.lam)
         graph = g
+        # what 8 GPUs would exchange: the same instance partitioned for 8 ranks x 147 CTAs (the
+        # layout ShardedResident / num_gpus=8 builds), peer-memory stores per rank per sweep
+        try:
+            from paper_2011_08170_b200 import _f2m
+            _f2m.set_sweep_partition(8 * 147)
+            try:
+                g8 = f2m.build_knn_graph(inst, K)
+            finally:
+                _f2m.set_sweep_partition(0)
+            tr = [_f2m.sweep_multi_traffic(g8, r, 8) for r in range(8)]
+            out["projection_8_ranks"] = {
+                "peer_bytes_per_sweep_per_rank_max": max(t["bytes_per_sweep"] for t in tr),
+                "peer_bytes_per_sweep_total": sum(t["bytes_per_sweep"] for t in tr),
+                "smem_resident": bool(_f2m.sweep_multi_info(g8, 0, 8)["resident"]),
+                "note": "16-byte LL stores of the boundary multipliers other ranks read + CTA sweep maxima"}
+            del g8
+        except Exception as exc:  # noqa: BLE001
+            out["projection_8_ranks"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     else:
         eng, err = _resident_engine(inst, comm)
         if eng is None:

@@ -209,7 +209,8 @@ __device__ __forceinline__ unsigned long long warp_max_nonneg_ap(double x) {
 
 // One TMA bulk prefetch of [p, p + bytes) into L2 (cp.async.bulk.prefetch.L2: 16-byte aligned
 // start and size, so the range is widened to 16-byte boundaries). The streaming sweep form issues
-// it a slice ahead per warp, the dense all-pairs form a row ahead.
+// it a slice ahead per warp. (A row-ahead prefetch in the dense all-pairs form over-fills L2 —
+// 4,736 warps x 64 KB rows — and re-fetches: 118 vs 92 us/sweep at n = 8,000, so it has none.)
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   if (!bytes) return;
   const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
@@ -249,8 +250,9 @@ struct AllPairsArgs {
 };
 
 // DENSE form: the n x n distance matrix is computed once per graph (k_dense_distances, the same
-// exact fp64 sequence) and every sweep streams row v (coalesced, L2-resident up to n ~ 3,900) instead
-// of recomputing the square roots — HBM / L2-bound instead of FP64-bound.
+// exact fp64 sequence) and every sweep streams row v (coalesced, 8 loads in flight per lane;
+// L2-resident up to n ~ 3,900) instead of recomputing the square roots — HBM / L2-bound instead of
+// FP64-bound.
 // D[p][q] = distance(point p, point q) in position order, distance()'s exact sequence
 // (instance.cpp:126-141: sqrt(dx*dx + dy*dy) without FMA, rounded mode floor(d + 0.5)) with dx taken
 // from the row's point as the recompute form does; symmetric bit for bit.
@@ -291,9 +293,6 @@ __global__ void __launch_bounds__(DENSE ? kDenseThreads : kAllPairsThreads, 1) k
       for (int i = 0; i <= B; ++i) s[i] = CUDART_INF;
       if (DENSE) {
         const double* __restrict__ row = a.dense + (size_t)v * a.n;
-        // the warp's next row into L2 (one TMA bulk prefetch) while this one streams
-        const int vn = v + gridDim.x * nwarps;
-        if (lane == 0 && vn < a.n) prefetch_l2(a.dense + (size_t)vn * a.n, (unsigned)a.n * 8u);
         int u = lane;
         for (; u + 224 < a.n; u += 256) {  // 8 coalesced row loads in flight per lane
           double c[8];
@@ -375,6 +374,9 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+#ifndef F2M_STREAM_BATCH
+#define F2M_STREAM_BATCH 6  // r02 A/B at 2M: 4 -> 52.0, 6 -> 46.5, 8 -> 49.1 us/sweep
+#endif
 #ifndef F2M_L2_PREFETCH_AHEAD
 #define F2M_L2_PREFETCH_AHEAD 1
 #endif
@@ -730,6 +732,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     return;
   }
   const int cthreads = ncw * 32;
+  // slots per batch of the row scans: 8 from shared memory; the streaming form's global loads
+  // are bounded by its 64-register budget at 1024 threads
+  constexpr int kBatch = RES ? 8 : F2M_STREAM_BATCH;
   const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
   const int p0 = s_lo * 32;
   const int own = max(0, min(s_hi * 32, a.n) - p0);
@@ -944,17 +949,17 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           // the warp's 32 lanes are the 32 rows of one boundary slice (bstart is slice-aligned):
           // one width, so the interior rows' 8-slot batches apply without predication
           int j = 0;
-          for (; j + 8 <= w; j += 8) {
-            int li[8];
-            double cs[8];
+          for (; j + kBatch <= w; j += kBatch) {
+            int li[kBatch];
+            double cs[kBatch];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kBatch; ++u) {
               const int idx = lb + 32 * (j + u);
               li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
               cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+            for (int u = 0; u < kBatch; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
           }
           for (; j < w; ++j) {
             const int idx = lb + 32 * j;
@@ -1000,17 +1005,17 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
       for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
       int j = 0;
-      for (; j + 8 <= w; j += 8) {
-        int li[8];
-        double cs[8];
+      for (; j + kBatch <= w; j += kBatch) {
+        int li[kBatch];
+        double cs[kBatch];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kBatch; ++u) {
           const int idx = lb + 32 * (j + u);
           li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
           cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+        for (int u = 0; u < kBatch; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
       }
       for (; j < w; ++j) {
         const int idx = lb + 32 * j;

@@ -431,6 +431,25 @@ def test_local_resident_ranks_100k_and_truncated():
 
 
 @pytest.mark.gpu
+def test_local_resident_8_ranks_2m_fixed_sweeps():
+    """BASELINE configs[4]'s shape through the torch-driven engine: 2M cities over 8 in-process
+    ranks (8 x 17 partition CTAs sharing the one GPU, streaming form), 64 fixed sweeps,
+    bit-exact against the one-GPU kernel's multipliers."""
+    import paper_2011_08170_b200 as f2m
+    from paper_2011_08170_b200.sharded import LocalComm, ShardedResident
+
+    inst = f2m.generate_instance(2_000_000, 1, 1000.0)
+    g = f2m.build_knn_graph(inst, 10)
+    st = f2m.make_initial_state(g)
+    f2m.jacobi_sweeps(g, st, 64)
+    del g
+    eng = ShardedResident(inst, 10, LocalComm(8))
+    lam, srep = eng.run(-1.0, 64)
+    assert srep["sweeps"] == 64 and not srep["converged"] and srep["world"] == 8
+    assert np.array_equal(lam, np.asarray(st.lam))
+
+
+@pytest.mark.gpu
 def test_nccl_world1_resident_matches_single_gpu():
     import torch.distributed as dist
 

@@ -30,7 +30,12 @@ for name, kind, n, seed, eps in CONFIGS:
     if n <= 200000:  # warm-up
         f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=200000, out_value=xo, out_duals=lo)
     t0 = time.perf_counter()
-    r = f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=400000, out_value=xo, out_duals=lo)
+    try:
+        r = f2m.full_solve_arrays(xy, k=10, eps=eps, max_sweeps=400000, out_value=xo, out_duals=lo)
+    except Exception as exc:  # the 2M instance: the reference's extraction cap
+        print(json.dumps({"config": name, "n": n, "wall_s": time.perf_counter() - t0,
+                          "error": f"{type(exc).__name__}: {exc}"[:300]}), flush=True)
+        continue
     wall = time.perf_counter() - t0
     ms, sw = f2m.last_sweep_kernel()
     print(json.dumps({"config": name, "n": n, "m": int(r["graph"].m), "wall_s": wall, "t_total": r["t_total"],
