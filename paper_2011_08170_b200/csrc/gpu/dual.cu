@@ -374,6 +374,9 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+#ifndef F2M_RES_BATCH
+#define F2M_RES_BATCH 4  // r02 A/B: 4 / 6 / 8 slots -> 100k 2.375 / 2.390 / 2.424 us, 200k 3.623 / 3.689 / 3.693
+#endif
 #ifndef F2M_STREAM_BATCH
 #define F2M_STREAM_BATCH 6  // r02 A/B at 2M: 4 -> 52.0, 6 -> 46.5, 8 -> 49.1 us/sweep
 #endif
@@ -734,7 +737,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   const int cthreads = ncw * 32;
   // slots per batch of the row scans: 8 from shared memory; the streaming form's global loads
   // are bounded by its 64-register budget at 1024 threads
-  constexpr int kBatch = RES ? 8 : F2M_STREAM_BATCH;
+  constexpr int kBatch = RES ? F2M_RES_BATCH : F2M_STREAM_BATCH;
   const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
   const int p0 = s_lo * 32;
   const int own = max(0, min(s_hi * 32, a.n) - p0);
