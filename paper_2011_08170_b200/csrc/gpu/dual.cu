@@ -735,8 +735,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     return;
   }
   const int cthreads = ncw * 32;
-  // slots per batch of the row scans: 8 from shared memory; the streaming form's global loads
-  // are bounded by its 64-register budget at 1024 threads
+  // slots per batch of the row scans: shared-memory scans keep few loads in flight (fewer live
+  // registers, less rematerialisation), the streaming form's global loads are bounded by its
+  // 64-register budget at 1024 threads (A/B figures at the macro definitions)
   constexpr int kBatch = RES ? F2M_RES_BATCH : F2M_STREAM_BATCH;
   const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
   const int p0 = s_lo * 32;
