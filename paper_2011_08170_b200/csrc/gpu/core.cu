@@ -599,18 +599,26 @@ static void build_local_index(Topology& t) {
   // boundary count and the per-CTA slice table size (v5: (slot offset, width) per slice, 16-byte
   // aligned) from one stream synchronisation
   int max_slices = 0;
+  int64_t max_lid4 = 0;  // resident: packed local indices, 4 slots per 8-byte entry, widths padded to 4
   {
     int32_t* hs = reinterpret_cast<int32_t*>(pinned_scratch());
     F2M_CUDA(cudaMemcpyAsync(hs, t.boff.get() + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> lo(G + 1);
+    std::vector<int32_t> lo(G + 1), wid(t.nslices);
     F2M_CUDA(cudaMemcpyAsync(lo.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(wid.data(), t.swidth.get(), sizeof(int32_t) * t.nslices, cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
     t.nboundary = hs[0];
-    for (int c = 0; c < G; ++c) max_slices = std::max(max_slices, lo[c + 1] - lo[c]);
+    for (int c = 0; c < G; ++c) {
+      max_slices = std::max(max_slices, lo[c + 1] - lo[c]);
+      int64_t l4 = 0;
+      for (int i = lo[c]; i < lo[c + 1]; ++i) l4 += 32 * ((wid[i] + 3) / 4);
+      max_lid4 = std::max(max_lid4, l4);
+    }
   }
-  const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int2);
-  const size_t resident_bytes = 2 * lam_aligned + ids_bytes +
-                                (size_t)t.max_cta_slots * (sizeof(double) + sizeof(uint16_t)) + slice_bytes;
+  t.max_cta_lid4 = max_lid4;
+  const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int4);
+  const size_t resident_bytes = 2 * lam_aligned + ids_bytes + (size_t)t.max_cta_slots * sizeof(double) +
+                                (size_t)max_lid4 * 8 + slice_bytes;
   const size_t streaming_bytes = lam_aligned + ids_bytes + slice_bytes;
   if (streaming_bytes > limit) return;  // v1 kernel
   // The sweep kernel keeps per-sweep CTA maxima in a ring of kCmaxRing (64) slots. A CTA starts

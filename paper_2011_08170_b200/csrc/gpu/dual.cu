@@ -466,6 +466,7 @@ struct Sweep4Args {
   double* record;
   int lam_stride;
   int halo_stride;           // ints of the halo LL-id region (max halo, multiple of 4)
+  int lid4_stride;           // resident: packed local-index entries (ushort4) per CTA (max)
   const int32_t* __restrict__ sdest;     // v5: slot -> halo-last slot
   unsigned poll_ns;          // v5: sync-warp back-off between unproductive halo polls
   int runahead;              // v5: stage the next sweep's halo while this sweep computes
@@ -715,6 +716,53 @@ __device__ __forceinline__ void publish_cmax(const Sweep4Args& a, size_t off, do
   for (int q = 0; q < a.npeers; ++q) st_ll_sys(a.cmax_peers[q] + off, v, tag);
 }
 
+// One row's scan over its slice's w slot columns (dual.cpp:33-61 smallest_adjusted for the lane's
+// row): reduced costs (c - l_v) - l_u through the top-(B+1) list, KB slots per batch. Resident:
+// costs and packed local indices from shared memory (l4 = this lane's packed-index column);
+// streaming: both from global memory with evict-first loads.
+template <int B, bool RES, int KB>
+__device__ __forceinline__ void row_scan(double (&sv)[B + 1], double lv, const double* lam,
+                                         const double* cst_s, const ushort4* l4, const double* __restrict__ gcost,
+                                         const uint16_t* __restrict__ glid, int lb, int w) {
+  int j = 0;
+  for (; j + KB <= w; j += KB) {
+    int li[KB];
+    double cs[KB];
+    if (RES) {
+      static_assert(!RES || KB % 4 == 0, "packed indices: batches of 4");
+#pragma unroll
+      for (int g = 0; g < KB / 4; ++g) {
+        const ushort4 q = l4[32 * ((j >> 2) + g)];
+        li[4 * g] = q.x;
+        li[4 * g + 1] = q.y;
+        li[4 * g + 2] = q.z;
+        li[4 * g + 3] = q.w;
+      }
+#pragma unroll
+      for (int u = 0; u < KB; ++u) cs[u] = cst_s[lb + 32 * (j + u)];
+    } else {
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        li[u] = __ldcs(glid + lb + 32 * (j + u));
+        cs[u] = __ldcs(gcost + lb + 32 * (j + u));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < KB; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
+  }
+  if (RES) {
+    if (j < w) {  // tail: 1-3 slots of the last packed group
+      const ushort4 q = l4[32 * (j >> 2)];
+      const int lt[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (j + u < w) topk_bubble<B>(sv, dsub(dsub(cst_s[lb + 32 * (j + u)], lv), lam[lt[u]]));
+    }
+  } else {
+    for (; j < w; ++j) topk_bubble<B>(sv, dsub(dsub(__ldcs(gcost + lb + 32 * j), lv), lam[__ldcs(glid + lb + 32 * j)]));
+  }
+}
+
 template <int B, bool RES, int NT, bool PAIR>
 __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -765,23 +813,40 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   double* regB = regA + (RES ? a.lam_stride : 0);
   int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
   double* cst_s = reinterpret_cast<double*>(halo_s + a.halo_stride);
-  uint16_t* lid_s = reinterpret_cast<uint16_t*>(cst_s + (RES ? nslots : 0));
-  // per-slice (slot offset, width) of this CTA: no global loads on the sweep path. The 16-byte
-  // alignment is computed on the offset from `smem` so the compiler keeps the shared address space
-  // (a uintptr_t round trip turned these into generic LD.E loads)
-  const size_t slc_off =
-      ((size_t)(reinterpret_cast<unsigned char*>(lid_s + (RES ? nslots : 0)) - smem) + 15) & ~size_t(15);
-  int2* slc = reinterpret_cast<int2*>(smem + slc_off);
+  // resident local indices, packed 4 slots per lane: slice t's slot (j, lane) is component j % 4 of
+  // lid4[slc[t].z + 32 (j / 4) + lane] — one 8-byte load per lane per 4 slots instead of four 2-byte
+  // loads (widths are padded to a multiple of 4 for this array only; the padding is never read)
+  ushort4* lid4 = reinterpret_cast<ushort4*>(cst_s + (RES ? nslots : 0));
+  const int nlid4 = RES ? a.lid4_stride : 0;
+  // per-slice {slot offset, width, packed-index offset} of this CTA: no global loads on the sweep
+  // path. The 16-byte alignment is computed on the offset from `smem` so the compiler keeps the
+  // shared address space (a uintptr_t round trip turned these into generic LD.E loads)
+  const size_t slc_off = ((size_t)(reinterpret_cast<unsigned char*>(lid4 + nlid4) - smem) + 15) & ~size_t(15);
+  int4* slc = reinterpret_cast<int4*>(smem + slc_off);
   const double* __restrict__ gcost = a.scost + slot0;
   const uint16_t* __restrict__ glid = a.slidx + slot0;
   for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
-  for (int i = tid; i < s_hi - s_lo; i += blockDim.x)
-    slc[i] = make_int2((int)(a.sptr[s_lo + i] - slot0), a.swidth[s_lo + i]);
+  if (tid == 0) {  // <= ~60 slices per CTA in the resident regime
+    int z = 0;
+    for (int i = 0; i < s_hi - s_lo; ++i) {
+      const int w = a.swidth[s_lo + i];
+      slc[i] = make_int4((int)(a.sptr[s_lo + i] - slot0), w, z, 0);
+      z += 32 * ((w + 3) >> 2);
+    }
+  }
   if (RES) {
+    __syncthreads();  // slice table in place
+    const int ns = s_hi - s_lo;
     for (int i = tid; i < nslots; i += blockDim.x) {  // rows stored own-first, halo-last
       const int d = (int)(a.sdest[slot0 + i] - slot0);
       cst_s[d] = gcost[i];
-      lid_s[d] = glid[i];
+      int t0 = 0, t1 = ns;  // slice holding destination slot d
+      while (t1 - t0 > 1) {
+        const int mid = (t0 + t1) >> 1;
+        if (slc[mid].x <= d) t0 = mid; else t1 = mid;
+      }
+      const int r = d - slc[t0].x, j = r >> 5;
+      reinterpret_cast<uint16_t*>(lid4)[(size_t)(slc[t0].z + 32 * (j >> 2) + (r & 31)) * 4 + (j & 3)] = glid[i];
     }
     for (int i = tid; i < own; i += blockDim.x) regA[i] = a.gl[p0 + i];
   }
@@ -897,9 +962,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         if (node < nbnd) {
           lp = bstart + node;
           p = p0 + lp;
-          const int2 sw2 = slc[(p >> 5) - s_lo];
+          const int4 sw2 = slc[(p >> 5) - s_lo];
           const int lb = sw2.x + (p & 31);
           const int w = sw2.y;
+          const uint16_t* lidr = reinterpret_cast<const uint16_t*>(lid4 + sw2.z + (p & 31));
           lv = lam[lp];
           for (int jj = half; jj < w; jj += 8) {
             int li[4];
@@ -907,8 +973,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const bool ok = jj + 2 * u < w;
-              const int idx = lb + 32 * (ok ? jj + 2 * u : 0);
-              li[u] = lid_s[idx];
+              const int jx = ok ? jj + 2 * u : 0;
+              const int idx = lb + 32 * jx;
+              li[u] = lidr[128 * (jx >> 2) + (jx & 3)];
               cs[u] = cst_s[idx];
               if (!ok) {
                 li[u] = lp;
@@ -942,7 +1009,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         const int node = base + brow;
         if (node < nbnd) {
           const int lp = bstart + node, p = p0 + lp;
-          const int2 sw2 = slc[(p >> 5) - s_lo];
+          const int4 sw2 = slc[(p >> 5) - s_lo];
           const int lb = sw2.x + (p & 31);
           const int w = sw2.y;
           double sv[B + 1];
@@ -951,26 +1018,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           const double lv = lam[lp];
           F2M_PROF_T(ta);
           // the warp's 32 lanes are the 32 rows of one boundary slice (bstart is slice-aligned):
-          // one width, so the interior rows' 8-slot batches apply without predication
-          int j = 0;
-          for (; j + kBatch <= w; j += kBatch) {
-            int li[kBatch];
-            double cs[kBatch];
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-              const int idx = lb + 32 * (j + u);
-              li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
-              cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
-            }
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
-          }
-          for (; j < w; ++j) {
-            const int idx = lb + 32 * j;
-            const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
-            const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
-            topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
-          }
+          // one width, so the interior rows' batches apply without predication
+          row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
           F2M_PROF_T(tb);
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
@@ -994,39 +1043,21 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         // this warp's slice F2M_L2_PREFETCH_AHEAD slices from now, or (near the end of the sweep)
         // its first slice of the next sweep: the slot arrays are the same every sweep
         const int nx = sl + kPrefetchAhead * ncw < s_int ? sl + kPrefetchAhead * ncw : s_lo + warp;
-        const int2 q = slc[nx - s_lo];
+        const int4 q = slc[nx - s_lo];
         prefetch_l2(gcost + q.x, (unsigned)q.y * 32u * 8u);
         prefetch_l2(glid + q.x, (unsigned)q.y * 32u * 2u);
       }
       const int p = sl * 32 + lane;
       if (p >= a.n) continue;
       const int lp = p - p0;
-      const int2 sw2 = slc[sl - s_lo];
+      const int4 sw2 = slc[sl - s_lo];
       const int lb = sw2.x + lane;
       const int w = sw2.y;
       const double lv = lam[lp];
       double sv[B + 1];
 #pragma unroll
       for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-      int j = 0;
-      for (; j + kBatch <= w; j += kBatch) {
-        int li[kBatch];
-        double cs[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int idx = lb + 32 * (j + u);
-          li[u] = RES ? lid_s[idx] : __ldcs(glid + idx);
-          cs[u] = RES ? cst_s[idx] : __ldcs(gcost + idx);
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) topk_bubble<B>(sv, dsub(dsub(cs[u], lv), lam[li[u]]));
-      }
-      for (; j < w; ++j) {
-        const int idx = lb + 32 * j;
-        const int li = RES ? lid_s[idx] : __ldcs(glid + idx);
-        const double cst = RES ? cst_s[idx] : __ldcs(gcost + idx);
-        topk_bubble<B>(sv, dsub(dsub(cst, lv), lam[li]));
-      }
+      row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
       const double d = delta_of<B>(sv, a.update);
       const double nl = dadd(lv, dmul(a.eta, d));
       gout[p] = nl;
@@ -1335,6 +1366,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.record = d_record;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
     a.halo_stride = (t.max_halo + 3) & ~3;
+    a.lid4_stride = (int)t.max_cta_lid4;
     a.cta_base = 0;
     a.g_total = G;
     a.npeers = 0;
@@ -2031,6 +2063,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.record = nullptr;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
     a.halo_stride = (t.max_halo + 3) & ~3;
+    a.lid4_stride = (int)t.max_cta_lid4;
     a.cta_base = rank * Gp;
     a.g_total = G;
     a.npeers = world;

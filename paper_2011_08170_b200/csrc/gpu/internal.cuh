@@ -158,6 +158,7 @@ struct Topology {
   int max_local = 0;           // max over CTAs of own + halo
   int max_halo = 0;            // max over CTAs of halo entries
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
+  int64_t max_cta_lid4 = 0;    // max over CTAs of packed local-index entries (ushort4, widths padded to 4)
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
   int partition_override = 0;  // > 0: partition CTA count for finalize_topology (multi-GPU replicas)
   ~Topology();
