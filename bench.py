@@ -187,7 +187,8 @@ def _agree(ok: bool) -> bool:
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return ok
-    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     return bool(t.item())
 

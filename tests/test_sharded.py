@@ -504,3 +504,36 @@ def test_gloo_gather_ranges_subgroup(tmp_path):
     want = np.array([i * 10 + (0 if i < 7 else 1) for i in range(11)], np.float64)
     for r in (1, 2):
         assert np.array_equal(np.load(f"{out}.{r}.npy"), want)
+
+
+def _agree_worker(rank, world, port, out_path):
+    import sys
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+
+        # a leg whose setup fails on rank 1 only: every rank must see "not ok" and skip together,
+        # and the next collective (the barrier) must still complete on all ranks
+        first = bench._agree(rank != 1)
+        second = bench._agree(True)
+        dist.barrier()
+        np.save(f"{out_path}.{rank}.npy", np.array([first, second]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_bench_agreement_skips_together(tmp_path):
+    """bench.py's cross-rank agreement before every multi-rank leg's collectives (world 3, gloo):
+    one failing rank makes all ranks skip the leg instead of leaving the others blocked."""
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "a")
+    mp.spawn(_agree_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    for r in range(3):
+        assert np.load(f"{out}.{r}.npy").tolist() == [False, True]
