@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128) k_knn_query(int n, int per_node, int roun
 // registers (fully unrolled insertion, no local memory). Same candidates, same (distance, id)
 // total order and the same ring-termination bound as k_knn_query -> identical lists.
 template <int K>
-__global__ void __launch_bounds__(128) k_knn_query_reg(int n, int rounded, const GridParams* __restrict__ gpp,
+__global__ void __launch_bounds__(128, 4) k_knn_query_reg(int n, int rounded, const GridParams* __restrict__ gpp,
                                                        const int32_t* __restrict__ off,
                                                        const int32_t* __restrict__ ids,
                                                        const double2* __restrict__ pts,
