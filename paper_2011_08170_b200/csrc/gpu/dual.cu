@@ -377,6 +377,9 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 #ifndef F2M_RES_BATCH
 #define F2M_RES_BATCH 4  // r02 A/B: 4 / 6 / 8 slots -> 100k 2.375 / 2.390 / 2.424 us, 200k 3.623 / 3.689 / 3.693
 #endif
+#ifndef F2M_STREAM_POLL
+#define F2M_STREAM_POLL 4  // r02 A/B (4 vs 8): 2M 44.6 vs 44.4, 1M 22.1 vs 22.6, 400k 9.03 vs 9.46 us; spill-free
+#endif
 #ifndef F2M_STREAM_BATCH
 #define F2M_STREAM_BATCH 6  // r02 A/B at 2M: 4 -> 52.0, 6 -> 46.5, 8 -> 49.1 us/sweep
 #endif
@@ -861,6 +864,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   if (warp >= sync0) {
     // ---- sync warps: stage the halo of sweep s (LL tag s; sweep 0: the initial multipliers)
     const int sw = warp - sync0;
+    // halo entries per lane per poll round: 8 in the resident form; the streaming form's
+    // 64-register budget (1024 threads) may favour fewer loads in flight
+    constexpr int kPB = RES ? 8 : F2M_STREAM_POLL;
     for (int s = 0;; ++s) {
       const int need = (RES && a.runahead) ? s - 1 : s;  // the region being filled is no longer read
       while (s_done < need && !s_exit) __nanosleep(32);
@@ -870,30 +876,30 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
       const uint64_t t0 = globaltimer_ns();
       bool quit = false;
-      for (int base = sw * 32; base < nh && !quit; base += 64 * 8) {
+      for (int base = sw * 32; base < nh && !quit; base += 64 * kPB) {
         unsigned pend = 0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b)
+        for (int b = 0; b < kPB; ++b)
           if (base + lane + 64 * b < nh) pend |= 1u << b;
         if (s == 0) {
-          double v[8];
+          double v[kPB];
 #pragma unroll
-          for (int b = 0; b < 8; ++b)
+          for (int b = 0; b < kPB; ++b)
             if (pend & (1u << b)) v[b] = __ldcg(gin + a.halo[h0 + base + lane + 64 * b]);
 #pragma unroll
-          for (int b = 0; b < 8; ++b)
+          for (int b = 0; b < kPB; ++b)
             if (pend & (1u << b)) lam[own + base + lane + 64 * b] = v[b];
           continue;
         }
         int it = 0;
         while (__any_sync(0xffffffffu, pend != 0)) {
           const unsigned pend_before = pend;
-          unsigned long long w0[8], w1[8];
+          unsigned long long w0[kPB], w1[kPB];
 #pragma unroll
-          for (int b = 0; b < 8; ++b)
+          for (int b = 0; b < kPB; ++b)
             if (pend & (1u << b)) ld_ll_raw(llin + 2 * halo_s[base + lane + 64 * b], w0[b], w1[b]);
 #pragma unroll
-          for (int b = 0; b < 8; ++b)
+          for (int b = 0; b < kPB; ++b)
             if ((pend & (1u << b)) && ll_ok(w0[b], w1[b], (unsigned)s)) {
               lam[own + base + lane + 64 * b] = ll_val(w0[b], w1[b]);
               pend &= ~(1u << b);

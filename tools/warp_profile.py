@@ -47,12 +47,4 @@ out["boundary_row_phases"] = {"setup": float(sub[..., 0][P[:, :nw, 7] > 0].mean(
                               "finish_publish": float(sub[..., 2][P[:, :nw, 7] > 0].mean())}
 out["cta_example"] = {"cta": c, "warps": [[round(float(x)) for x in per[c, w]] + [int(P[c, w, 5]), int(P[c, w, 6]), int(P[c, w, 7])] + [round(float(x)) for x in sub[c, w]]
                                          for w in range(nw)]}
-# the two sync warps (22, 23): halo polling
-S = P[:, 22:24, :]
-sw_ = np.maximum(S[..., 3], 1)
-out["sync_warps"] = {"polls_per_sweep": float((S[..., 0] / sw_).mean()),
-                     "poll_round_cycles": float((S[..., 2] / np.maximum(S[..., 0], 1)).mean()),
-                     "polling_cycles_per_sweep": float((S[..., 1] / sw_).mean()),
-                     "gate_wait_cycles_per_sweep": float((S[..., 4] / sw_).mean()),
-                     "empty_polls_per_sweep": float((S[..., 5] / sw_).mean())}
 print(json.dumps(out))
