@@ -103,18 +103,31 @@ __global__ void k_heads(int64_t z, const uint64_t* __restrict__ keys, int ebits,
 }
 
 // solve_zero_component (primal.cpp:65-140) as an iterative DFS with the recursion's exact
-// visiting order and pruning. comp: edge ids (ascending). Returns false if infeasible.
-__device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __restrict__ eu,
+// visiting order and pruning. The search can be split: `depth` leading edges are forced to the
+// base-3 digits of `prefix` (edge 0 most significant) and only that subtree is searched, with its
+// own incumbent. The DFS keeps the FIRST leaf (in DFS = lexicographic order of the halves) that
+// reaches the subtree's minimum — a later leaf of equal cost is pruned by `cost >= best` — so the
+// whole search's answer is the minimum over subtrees of (cost, prefix): what k_components' warp
+// reduction takes. Returns the subtree's best cost (+inf: none) and its halves in best[].
+struct ZeroComponent {
+  int mc, nn;
+  int ce[kMaxComponentEdges];
+  int ea[kMaxComponentEdges], eb[kMaxComponentEdges];
+  double c[kMaxComponentEdges];
+  int target[2 * kMaxComponentEdges];  // 2 x residual per local node
+};
+
+__device__ void component_setup(ZeroComponent& z, const int32_t* comp, int mc, const int32_t* __restrict__ eu,
                                 const int32_t* __restrict__ ev, const double* __restrict__ cost,
-                                const int32_t* __restrict__ residual, double* __restrict__ x,
-                                bool comp_is_sorted_keys, const uint64_t* keys, int ebits) {
+                                const int32_t* __restrict__ residual, bool comp_is_sorted_keys,
+                                const uint64_t* keys, int ebits) {
   int nodes[2 * kMaxComponentEdges];
   int nn = 0;
-  int ce[kMaxComponentEdges];
+  z.mc = mc;
   for (int i = 0; i < mc; ++i) {
-    ce[i] = comp_is_sorted_keys ? (int)(keys[i] & ((1ull << ebits) - 1)) : comp[i];
-    nodes[nn++] = eu[ce[i]];
-    nodes[nn++] = ev[ce[i]];
+    z.ce[i] = comp_is_sorted_keys ? (int)(keys[i] & ((1ull << ebits) - 1)) : comp[i];
+    nodes[nn++] = eu[z.ce[i]];
+    nodes[nn++] = ev[z.ce[i]];
   }
   for (int i = 1; i < nn; ++i) {  // sort + unique (primal.cpp:73-75)
     const int v = nodes[i];
@@ -126,30 +139,51 @@ __device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __re
   for (int i = 0; i < nn; ++i)
     if (i == 0 || nodes[i] != nodes[i - 1]) nodes[u++] = nodes[i];
   nn = u;
+  z.nn = nn;
   auto local = [&](int v) {
     int lo = 0, hi = nn;
     while (lo < hi) { const int mid = (lo + hi) >> 1; if (nodes[mid] < v) lo = mid + 1; else hi = mid; }
     return lo;
   };
-  int target[2 * kMaxComponentEdges], rem[2 * kMaxComponentEdges];
-  int ea[kMaxComponentEdges], eb[kMaxComponentEdges];
-  double c[kMaxComponentEdges];
-  int halves[kMaxComponentEdges], best[kMaxComponentEdges];
-  for (int i = 0; i < nn; ++i) { target[i] = 2 * residual[nodes[i]]; rem[i] = 0; }
+  for (int i = 0; i < nn; ++i) z.target[i] = 2 * residual[nodes[i]];
   for (int i = 0; i < mc; ++i) {
-    ea[i] = local(eu[ce[i]]);
-    eb[i] = local(ev[ce[i]]);
-    ++rem[ea[i]];
-    ++rem[eb[i]];
-    c[i] = cost[ce[i]];
-    halves[i] = 0;
+    z.ea[i] = local(eu[z.ce[i]]);
+    z.eb[i] = local(ev[z.ce[i]]);
+    z.c[i] = cost[z.ce[i]];
   }
-  double best_cost = CUDART_INF;
+}
+
+__device__ double component_search(const ZeroComponent& z, int depth, int prefix, int* best) {
+  const int mc = z.mc;
+  int target[2 * kMaxComponentEdges], rem[2 * kMaxComponentEdges];
+  int halves[kMaxComponentEdges];
   double cst[kMaxComponentEdges + 1];
   int hh[kMaxComponentEdges + 1];
-  enum { ENTER, LOOP, RETURN };
-  int i = 0, state = ENTER;
+  for (int i = 0; i < z.nn; ++i) { target[i] = z.target[i]; rem[i] = 0; }
+  for (int i = 0; i < mc; ++i) {
+    ++rem[z.ea[i]];
+    ++rem[z.eb[i]];
+    halves[i] = 0;
+  }
+  // the forced prefix: the same checks the DFS applies on its way down (LOOP below)
   cst[0] = 0.0;
+  int pw = 1;
+  for (int i = 1; i < depth; ++i) pw *= 3;
+  for (int i = 0; i < depth; ++i, pw /= 3) {
+    const int h = (prefix / pw) % 3, a = z.ea[i], b = z.eb[i];
+    --rem[a];
+    --rem[b];
+    if (h > target[a] || h > target[b]) return CUDART_INF;
+    target[a] -= h;
+    target[b] -= h;
+    if (!(target[a] <= 2 * rem[a] && target[b] <= 2 * rem[b])) return CUDART_INF;
+    halves[i] = h;
+    hh[i] = h;
+    cst[i + 1] = dadd(cst[i], dmul(dmul(0.5, (double)h), z.c[i]));  // cost + 0.5*h*c
+  }
+  double best_cost = CUDART_INF;
+  enum { ENTER, LOOP, RETURN };
+  int i = depth, state = ENTER;
   for (;;) {
     if (state == ENTER) {
       if (cst[i] >= best_cost) {
@@ -159,15 +193,15 @@ __device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __re
         for (int k = 0; k < mc; ++k) best[k] = halves[k];
         state = RETURN;
       } else {
-        --rem[ea[i]];
-        --rem[eb[i]];
+        --rem[z.ea[i]];
+        --rem[z.eb[i]];
         hh[i] = 0;
         state = LOOP;
       }
     }
     if (state == LOOP) {
       bool descend = false;
-      const int a = ea[i], b = eb[i];
+      const int a = z.ea[i], b = z.eb[i];
       while (hh[i] <= 2) {
         const int h = hh[i];
         if (h > target[a] || h > target[b]) { hh[i] = 3; break; }
@@ -175,7 +209,7 @@ __device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __re
         target[b] -= h;
         if (target[a] <= 2 * rem[a] && target[b] <= 2 * rem[b]) {
           halves[i] = h;
-          cst[i + 1] = dadd(cst[i], dmul(dmul(0.5, (double)h), c[i]));  // cost + 0.5*h*c
+          cst[i + 1] = dadd(cst[i], dmul(dmul(0.5, (double)h), z.c[i]));  // cost + 0.5*h*c
           descend = true;
           break;
         }
@@ -188,35 +222,75 @@ __device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __re
       ++rem[b];
       state = RETURN;
     }
-    // RETURN to the caller frame
-    if (i == 0) break;
+    // RETURN to the caller frame (never above the forced prefix)
+    if (i == depth) break;
     --i;
-    target[ea[i]] += hh[i];
-    target[eb[i]] += hh[i];
+    target[z.ea[i]] += hh[i];
+    target[z.eb[i]] += hh[i];
     ++hh[i];
     state = LOOP;
   }
-  if (!(best_cost < CUDART_INF)) return false;  // !isfinite(best_cost)
-  for (int k = 0; k < mc; ++k) x[ce[k]] = 0.5 * best[k];
+  return best_cost;
+}
+
+// The whole tree on one thread (k_one_component, the solve_zero_component entry point).
+__device__ bool solve_component(const int32_t* comp, int mc, const int32_t* __restrict__ eu,
+                                const int32_t* __restrict__ ev, const double* __restrict__ cost,
+                                const int32_t* __restrict__ residual, double* __restrict__ x,
+                                bool comp_is_sorted_keys, const uint64_t* keys, int ebits) {
+  ZeroComponent z;
+  component_setup(z, comp, mc, eu, ev, cost, residual, comp_is_sorted_keys, keys, ebits);
+  int best[kMaxComponentEdges];
+  if (!(component_search(z, 0, 0, best) < CUDART_INF)) return false;  // !isfinite(best_cost)
+  for (int k = 0; k < mc; ++k) x[z.ce[k]] = 0.5 * best[k];
   return true;
 }
 
+// One warp per zero component: the search tree is split at its first 3 edges into 27 subtrees,
+// one per lane, and the lanes' (cost, prefix) minimum is the sequential search's answer
+// (see component_search). The exhaustive search of the largest component set this kernel's time
+// on one thread (130 us at 100k).
+constexpr int kSplitDepth = 3;
 __global__ void k_components(int64_t ncomp, int64_t z, const int32_t* __restrict__ heads,
                              const uint64_t* __restrict__ keys, const int32_t* __restrict__ eu,
                              const int32_t* __restrict__ ev, const double* __restrict__ cost,
                              const int32_t* __restrict__ residual, double* __restrict__ x, int ebits,
                              unsigned long long* __restrict__ fail) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= ncomp) return;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= ncomp) return;  // warp-uniform
   const int64_t lo = heads[c], hi = c + 1 < ncomp ? heads[c + 1] : z;
   const int64_t mc = hi - lo;
   if (mc > kMaxComponentEdges) {  // primal.cpp:210-214
-    atomicMin(fail, ((unsigned long long)c << 32) | (unsigned long long)mc);
+    if (lane == 0) atomicMin(fail, ((unsigned long long)c << 32) | (unsigned long long)mc);
     return;
   }
-  if (!solve_component(nullptr, (int)mc, eu, ev, cost, residual, x, true, keys + lo, ebits)) {
-    atomicMin(fail, ((unsigned long long)c << 32) | (unsigned long long)(0x80000000u | (unsigned)mc));
+  ZeroComponent zc;
+  component_setup(zc, nullptr, (int)mc, eu, ev, cost, residual, true, keys + lo, ebits);
+  const int depth = mc < kSplitDepth ? (int)mc : kSplitDepth;
+  const int nprefix = depth == 3 ? 27 : depth == 2 ? 9 : depth == 1 ? 3 : 1;
+  int best[kMaxComponentEdges];
+  double bc = CUDART_INF;
+  int bp = 0x7fffffff;
+  if (lane < nprefix) {
+    bc = component_search(zc, depth, lane, best);
+    bp = lane;
   }
+  // lexicographic (cost, prefix) minimum over the lanes; NaN costs never win (as in the DFS)
+  double wc = bc;
+  int wp = bc < CUDART_INF ? bp : 0x7fffffff;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const double oc = __shfl_xor_sync(0xffffffffu, wc, off);
+    const int op = __shfl_xor_sync(0xffffffffu, wp, off);
+    if (oc < wc || (oc == wc && op < wp)) { wc = oc; wp = op; }
+  }
+  if (!(wc < CUDART_INF)) {
+    if (lane == 0) atomicMin(fail, ((unsigned long long)c << 32) | (unsigned long long)(0x80000000u | (unsigned)mc));
+    return;
+  }
+  if (lane == wp)
+    for (int k = 0; k < mc; ++k) x[zc.ce[k]] = 0.5 * best[k];
 }
 
 __global__ void k_one_component(int mc, const int32_t* __restrict__ comp, const int32_t* __restrict__ eu,
@@ -360,8 +434,8 @@ void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, dou
   const int64_t ncomp = select_flagged<int32_t>(zi.get(), head.get(), heads.get(), z, s);
   DBuf<unsigned long long> fail(1, s);
   F2M_CUDA(cudaMemsetAsync(fail.get(), 0xff, sizeof(unsigned long long), s));
-  k_components<<<grid_for(ncomp, 64), 64, 0, s>>>(ncomp, z, heads.get(), k1.get(), t.eu.get(), t.ev.get(),
-                                                  g.cost.get(), residual.get(), d_x, ebits, fail.get());
+  k_components<<<grid_for(ncomp * 32, 128), 128, 0, s>>>(ncomp, z, heads.get(), k1.get(), t.eu.get(), t.ev.get(),
+                                                        g.cost.get(), residual.get(), d_x, ebits, fail.get());
   launched("zero_components");
   unsigned long long hf = 0;
   F2M_CUDA(cudaMemcpyAsync(&hf, fail.get(), sizeof(hf), cudaMemcpyDeviceToHost, s));
