@@ -766,6 +766,140 @@ __device__ __forceinline__ void row_scan(double (&sv)[B + 1], double lv, const d
   }
 }
 
+#ifndef F2M_HEAD_SCAN
+#define F2M_HEAD_SCAN 1
+#endif
+#ifdef F2M_HEAD_TIMING_NORESCAN  // TIMING ONLY (wrong results): the rescan path compiled but never taken
+#define F2M_HEAD_NORESCAN && a.poll_ns == 0xdeadbeefu
+#else
+#define F2M_HEAD_NORESCAN
+#endif
+#ifdef F2M_HEAD_STATS  // debug build: repaired rows, printed at exit
+__device__ unsigned long long g_head_stats[4];
+#define F2M_HEAD_COUNT(i) atomicAdd(&g_head_stats[i], 1ull)
+#else
+#define F2M_HEAD_COUNT(i)
+#endif
+
+// Resident row scan with a "head" of B+2 slots: the row's B+2 smallest slots of an earlier sweep,
+// kept first in the row's shared-memory slot order. A row's smallest reduced costs almost never
+// change membership from one sweep to the next (uniform 10k, per sweep: the top-(B+1) set of 0.09 %
+// of rows changes, but only 0.014 % of rows see a slot from outside the previous top-(B+2) enter
+// the top-(B+1); tools/head_stability.py), so:
+//  * the head's B+2 reduced costs are sorted directly (a sorting network);
+//  * every tail slot is only COMPARED with the (B+1)-th smallest head value: 2 DADD + 1 DSETP per
+//    slot, no selects and no loop-carried chain, so the loads of all batches overlap;
+//  * a row whose tail has a value below it is rescanned by the plain insertion (row_scan,
+//    dual.cpp:44-58 smallest_adjusted) and row_repair moves its new B+2 smallest slots to the head.
+// The kept multiset — the B+1 smallest reduced costs of the row — does not depend on the visiting
+// order (reduced costs are never -0.0: costs are >= +0 and x - y = -0 only for x = -0), so s[B-1],
+// s[B] and hence delta are bit-identical to the plain insertion over all slots.
+// Returns true when the row must be rescanned.
+template <int B>
+__device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, const double* lam,
+                                              const double* cst_s, const ushort4* l4, int lb, int w) {
+  constexpr int H = B + 2;
+  constexpr int HG = (H + 3) / 4;  // packed-index groups covering the head
+  int li[4 * HG];
+#pragma unroll
+  for (int g = 0; g < HG; ++g) {
+    const ushort4 q = l4[32 * g];
+    li[4 * g] = q.x;
+    li[4 * g + 1] = q.y;
+    li[4 * g + 2] = q.z;
+    li[4 * g + 3] = q.w;
+  }
+#pragma unroll
+  for (int h = 0; h < H; ++h) sv[h] = dsub(dsub(cst_s[lb + 32 * h], lv), lam[li[h]]);
+  auto cas = [&](int i, int k) {
+    const bool sw = sv[k] < sv[i];
+    const double lo = sw ? sv[k] : sv[i];
+    sv[k] = sw ? sv[i] : sv[k];
+    sv[i] = lo;
+  };
+  if (H == 4) {  // b = 2: the optimal 5-comparator network
+    cas(0, 1);
+    cas(2, 3);
+    cas(0, 2);
+    cas(1, 3);
+    cas(1, 2);
+  } else {  // odd-even transposition
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+#pragma unroll
+      for (int i = r & 1; i + 1 < H; i += 2) cas(i, i + 1);
+    }
+  }
+  const double thr = sv[B];
+  bool hit = false;
+  int j = H;
+#ifdef F2M_TIMING_F32TAIL  // TIMING ONLY (wrong results): tail compares on 4-byte costs / multipliers
+  const float* c32 = reinterpret_cast<const float*>(cst_s);
+  const float* l32 = reinterpret_cast<const float*>(lam);
+  const float lv32 = (float)lv, thr32 = (float)thr;
+#define F2M_TAILV(jj, idx) (__fsub_rn(__fsub_rn(c32[lb + 32 * (jj)], lv32), l32[idx]) < thr32)
+#else
+#define F2M_TAILV(jj, idx) (dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[idx]) < thr)
+#endif
+  if (H % 4) {  // tail slots of the last head group
+#pragma unroll
+    for (int u = 0; u < (4 - H % 4) % 4; ++u)
+      if (j + u < w) hit |= F2M_TAILV(j + u, li[4 * HG - (4 - H % 4) + u]);
+    j = 4 * HG;
+  }
+  for (; j + 4 <= w; j += 4) {
+    const ushort4 q = l4[32 * (j >> 2)];
+    const int lt[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) hit |= F2M_TAILV(j + u, lt[u]);
+  }
+  if (j < w) {  // 1-3 slots of the last packed group
+    const ushort4 q = l4[32 * (j >> 2)];
+    const int lt[3] = {q.x, q.y, q.z};
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (j + u < w) hit |= F2M_TAILV(j + u, lt[u]);
+  }
+#undef F2M_TAILV
+  return hit;
+}
+
+// Moves the row's K+1 smallest slots (values < s[K], then as many == s[K] as the list holds) to the
+// head of its shared-memory slot order: a stable partition over the same frozen snapshot. Only
+// the owning thread reads or writes a row's slots.
+template <int K>
+__device__ __forceinline__ void row_repair(const double (&sv)[K + 1], double lv, const double* lam, double* cst_s,
+                                           ushort4* l4, int lb, int w) {
+  uint16_t* lid = reinterpret_cast<uint16_t*>(l4);
+  F2M_HEAD_COUNT(1);
+  const double thr = sv[K];
+  int needeq = 0;
+#pragma unroll
+  for (int i = 0; i <= K; ++i) needeq += !(sv[i] < thr);
+  int cnt = 0;
+  for (int j = 0; j < w && cnt <= K; ++j) {
+    const int xj = 128 * (j >> 2) + (j & 3);
+    const uint16_t ij = lid[xj];
+    const double cj = cst_s[lb + 32 * j];
+    const double v = dsub(dsub(cj, lv), lam[ij]);
+    bool take = v < thr;
+    if (!take && v == thr && needeq > 0) {
+      take = true;
+      --needeq;
+    }
+    if (take) {
+      if (j != cnt) {
+        const int xc = 128 * (cnt >> 2) + (cnt & 3);
+        lid[xj] = lid[xc];
+        cst_s[lb + 32 * j] = cst_s[lb + 32 * cnt];
+        lid[xc] = ij;
+        cst_s[lb + 32 * cnt] = cj;
+      }
+      ++cnt;
+    }
+  }
+}
+
 template <int B, bool RES, int NT, bool PAIR>
 __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -790,6 +924,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // registers, less rematerialisation), the streaming form's global loads are bounded by its
   // 64-register budget at 1024 threads (A/B figures at the macro definitions)
   constexpr int kBatch = RES ? F2M_RES_BATCH : F2M_STREAM_BATCH;
+  constexpr bool kHead = RES && F2M_HEAD_SCAN;  // head-first row scans (row_scan_head)
   const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
   const int p0 = s_lo * 32;
   const int own = max(0, min(s_hi * 32, a.n) - p0);
@@ -1025,7 +1160,19 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           F2M_PROF_T(ta);
           // the warp's 32 lanes are the 32 rows of one boundary slice (bstart is slice-aligned):
           // one width, so the interior rows' batches apply without predication
-          row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
+          if (kHead && w > B + 1) {
+            double hv[B + 2];
+            if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), lb, w) F2M_HEAD_NORESCAN) {
+#pragma unroll
+              for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
+              row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
+              row_repair<B + 1>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), lb, w);
+            }
+#pragma unroll
+            for (int i = 0; i <= B; ++i) sv[i] = hv[i];
+          } else {
+            row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
+          }
           F2M_PROF_T(tb);
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
@@ -1063,7 +1210,19 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       double sv[B + 1];
 #pragma unroll
       for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-      row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
+      if (kHead && w > B + 1) {
+        double hv[B + 2];
+        if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w) F2M_HEAD_NORESCAN) {
+#pragma unroll
+          for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
+          row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
+          row_repair<B + 1>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w);
+        }
+#pragma unroll
+        for (int i = 0; i <= B; ++i) sv[i] = hv[i];
+      } else {
+        row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
+      }
       const double d = delta_of<B>(sv, a.update);
       const double nl = dadd(lv, dmul(a.eta, d));
       gout[p] = nl;
@@ -1127,6 +1286,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   }
 #endif
   if (tid == 0) s_exit = 1;
+#ifdef F2M_HEAD_STATS
+  if (tid == 0 && c == 0)
+    printf("head stats: repaired rows %llu\n", g_head_stats[1]);
+#endif
 }
 
 template <int B, bool RES, int NT, bool PAIR>

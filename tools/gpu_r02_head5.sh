@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python tools/ab_sweep.py exp/base exp/norescan exp/f32tail . --n 100000 --sweeps 3000 --reps 3 < /dev/null > gpurun_out/head5.log 2>&1
+timeout 900 python tools/ab_sweep.py exp/base exp/norescan exp/f32tail . --n 200000 --sweeps 3000 --reps 2 < /dev/null >> gpurun_out/head5.log 2>&1
+cat gpurun_out/head5.log
