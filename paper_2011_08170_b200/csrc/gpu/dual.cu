@@ -769,6 +769,14 @@ __device__ __forceinline__ void row_scan(double (&sv)[B + 1], double lv, const d
 #ifndef F2M_HEAD_SCAN
 #define F2M_HEAD_SCAN 1
 #endif
+#ifndef F2M_BANK_LAYOUT
+#define F2M_BANK_LAYOUT 1  // bank-aware initial slot order of the resident rows (layout_banks)
+#endif
+#ifdef F2M_T_CF  // TIMING ONLY (wrong results): bank-conflict-free multiplier gathers in the head scans
+#define F2M_LIDX(q_) (((q_) & ~15) | (threadIdx.x & 15))
+#else
+#define F2M_LIDX(q_) (q_)
+#endif
 #ifdef F2M_HEAD_TIMING_NORESCAN  // TIMING ONLY (wrong results): the rescan path compiled but never taken
 #define F2M_HEAD_NORESCAN && a.poll_ns == 0xdeadbeefu
 #else
@@ -810,7 +818,7 @@ __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, co
     li[4 * g + 3] = q.w;
   }
 #pragma unroll
-  for (int h = 0; h < H; ++h) sv[h] = dsub(dsub(cst_s[lb + 32 * h], lv), lam[li[h]]);
+  for (int h = 0; h < H; ++h) sv[h] = dsub(dsub(cst_s[lb + 32 * h], lv), lam[F2M_LIDX(li[h])]);
   auto cas = [&](int i, int k) {
     const bool sw = sv[k] < sv[i];
     const double lo = sw ? sv[k] : sv[i];
@@ -839,7 +847,7 @@ __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, co
   const float lv32 = (float)lv, thr32 = (float)thr;
 #define F2M_TAILV(jj, idx) (__fsub_rn(__fsub_rn(c32[lb + 32 * (jj)], lv32), l32[idx]) < thr32)
 #else
-#define F2M_TAILV(jj, idx) (dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[idx]) < thr)
+#define F2M_TAILV(jj, idx) (dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[F2M_LIDX(idx)]) < thr)
 #endif
   if (H % 4) {  // tail slots of the last head group
 #pragma unroll
@@ -896,6 +904,75 @@ __device__ __forceinline__ void row_repair(const double (&sv)[K + 1], double lv,
         cst_s[lb + 32 * cnt] = cj;
       }
       ++cnt;
+    }
+  }
+}
+
+// Initial slot order of one row (resident form, kernel setup): its B+2 smallest reduced costs at
+// the initial multipliers (lam0: own + staged halo) go to columns 0..B+1, the head of
+// row_scan_head. sl = {slot offset, width, packed-index offset} of the row's slice, l = its lane.
+__device__ __noinline__ void layout_head(int B, double* cst_s, ushort4* lid4, int4 sl, int l, double lv,
+                                         const double* lam0) {
+  uint16_t* lid = reinterpret_cast<uint16_t*>(lid4);
+  const int w = sl.y;
+  auto ix = [&](int k) { return (sl.z + 32 * (k >> 2) + l) * 4 + (k & 3); };
+  for (int h = 0; h < B + 2 && h < w; ++h) {  // selection: the smallest of columns h.. to column h
+    int best = h;
+    double bv = dsub(dsub(cst_s[sl.x + l + 32 * h], lv), lam0[lid[ix(h)]]);
+    for (int k = h + 1; k < w; ++k) {
+      const double v = dsub(dsub(cst_s[sl.x + l + 32 * k], lv), lam0[lid[ix(k)]]);
+      if (v < bv) {
+        bv = v;
+        best = k;
+      }
+    }
+    if (best != h) {
+      const uint16_t t = lid[ix(h)];
+      lid[ix(h)] = lid[ix(best)];
+      lid[ix(best)] = t;
+      const double c = cst_s[sl.x + l + 32 * h];
+      cst_s[sl.x + l + 32 * h] = cst_s[sl.x + l + 32 * best];
+      cst_s[sl.x + l + 32 * best] = c;
+    }
+  }
+}
+
+// Bank-aware column order of one half-slice (the 16 rows one half-warp scans together; a 64-bit
+// shared-memory load is served per half-warp, one 8-byte word per bank pair = local index mod 16).
+// Column by column, each row takes the first of its remaining slots whose multiplier word falls in
+// a bank pair no earlier row of the half-warp uses in that column, or is the same word (a
+// broadcast); a row with no such slot keeps its slot. Head columns (0..B+1) only permute among
+// themselves. Order only: the scans' results do not depend on it. Rows [l0, l0 + nrows) of the
+// slice sl.
+__device__ __noinline__ void layout_banks(int B, double* cst_s, ushort4* lid4, int4 sl, int l0, int nrows) {
+  uint16_t* lid = reinterpret_cast<uint16_t*>(lid4);
+  const int w = sl.y, H = w > B + 1 ? B + 2 : 0;
+  for (int j = 0; j < w; ++j) {
+    const int hi = j < H ? H : w;
+    unsigned used = 0;
+    uint16_t word[16];
+    for (int l = l0; l < l0 + nrows; ++l) {
+      int pick = j;
+      for (int k = j; k < hi; ++k) {
+        const uint16_t q = lid[(sl.z + 32 * (k >> 2) + l) * 4 + (k & 3)];
+        if (!((used >> (q & 15)) & 1u) || word[q & 15] == q) {
+          pick = k;
+          break;
+        }
+      }
+      const int xj = (sl.z + 32 * (j >> 2) + l) * 4 + (j & 3);
+      if (pick != j) {
+        const int xp = (sl.z + 32 * (pick >> 2) + l) * 4 + (pick & 3);
+        const uint16_t t = lid[xj];
+        lid[xj] = lid[xp];
+        lid[xp] = t;
+        const double c = cst_s[sl.x + l + 32 * j];
+        cst_s[sl.x + l + 32 * j] = cst_s[sl.x + l + 32 * pick];
+        cst_s[sl.x + l + 32 * pick] = c;
+      }
+      const uint16_t q = lid[xj];
+      used |= 1u << (q & 15);
+      word[q & 15] = q;
     }
   }
 }
@@ -987,6 +1064,18 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       reinterpret_cast<uint16_t*>(lid4)[(size_t)(slc[t0].z + 32 * (j >> 2) + (r & 31)) * 4 + (j & 3)] = glid[i];
     }
     for (int i = tid; i < own; i += blockDim.x) regA[i] = a.gl[p0 + i];
+    if (kHead && F2M_BANK_LAYOUT) {
+      // initial slot order: heads at the initial multipliers (halo staged here once), then
+      // bank-aware columns
+      for (int i = tid; i < nh; i += blockDim.x) regA[own + i] = __ldcg(a.gl + a.halo[h0 + i]);
+      __syncthreads();
+      for (int lp = tid; lp < own; lp += blockDim.x) layout_head(B, cst_s, lid4, slc[lp >> 5], lp & 31, regA[lp], regA);
+      __syncthreads();
+      for (int hs = tid; hs < 2 * ns; hs += blockDim.x) {  // one thread per half-slice
+        const int l0 = 16 * (hs & 1), nrows = min(16, own - 32 * (hs >> 1) - l0);
+        if (nrows > 0) layout_banks(B, cst_s, lid4, slc[hs >> 1], l0, nrows);
+      }
+    }
   }
   if (tid == 0) {
     s_word = 0ull;
