@@ -783,7 +783,7 @@ __device__ __forceinline__ void row_scan(double (&sv)[B + 1], double lv, const d
 #define F2M_HEAD_NORESCAN
 #endif
 #ifdef F2M_HEAD_STATS  // debug build: repaired rows, printed at exit
-__device__ unsigned long long g_head_stats[4];
+__device__ unsigned long long g_head_stats[8];
 #define F2M_HEAD_COUNT(i) atomicAdd(&g_head_stats[i], 1ull)
 #else
 #define F2M_HEAD_COUNT(i)
@@ -941,38 +941,71 @@ __device__ __noinline__ void layout_head(int B, double* cst_s, ushort4* lid4, in
 // shared-memory load is served per half-warp, one 8-byte word per bank pair = local index mod 16).
 // Column by column, each row takes the first of its remaining slots whose multiplier word falls in
 // a bank pair no earlier row of the half-warp uses in that column, or is the same word (a
-// broadcast); a row with no such slot keeps its slot. Head columns (0..B+1) only permute among
-// themselves. Order only: the scans' results do not depend on it. Rows [l0, l0 + nrows) of the
-// slice sl.
+// broadcast). A row with no such slot tries a one-step augmenting path: a bank pair it can reach
+// whose single user can move to a free pair. Otherwise it keeps its slot (a conflict). Head columns
+// (0..B+1) only permute among themselves. Order only: the scans' results do not depend on it.
+// Rows [l0, l0 + nrows) of the slice sl.
 __device__ __noinline__ void layout_banks(int B, double* cst_s, ushort4* lid4, int4 sl, int l0, int nrows) {
   uint16_t* lid = reinterpret_cast<uint16_t*>(lid4);
   const int w = sl.y, H = w > B + 1 ? B + 2 : 0;
+  auto ix = [&](int l, int k) { return (sl.z + 32 * (k >> 2) + l) * 4 + (k & 3); };
+  auto swap_cols = [&](int l, int j, int k) {
+    const int xj = ix(l, j), xk = ix(l, k);
+    const uint16_t t = lid[xj];
+    lid[xj] = lid[xk];
+    lid[xk] = t;
+    const double c = cst_s[sl.x + l + 32 * j];
+    cst_s[sl.x + l + 32 * j] = cst_s[sl.x + l + 32 * k];
+    cst_s[sl.x + l + 32 * k] = c;
+  };
   for (int j = 0; j < w; ++j) {
     const int hi = j < H ? H : w;
-    unsigned used = 0;
+    unsigned used = 0, shared = 0;  // bank pairs in use / used by more than one row (a broadcast)
     uint16_t word[16];
+    int8_t owner[16];
     for (int l = l0; l < l0 + nrows; ++l) {
-      int pick = j;
+      int pick = -1;
       for (int k = j; k < hi; ++k) {
-        const uint16_t q = lid[(sl.z + 32 * (k >> 2) + l) * 4 + (k & 3)];
+        const uint16_t q = lid[ix(l, k)];
         if (!((used >> (q & 15)) & 1u) || word[q & 15] == q) {
           pick = k;
           break;
         }
       }
-      const int xj = (sl.z + 32 * (j >> 2) + l) * 4 + (j & 3);
-      if (pick != j) {
-        const int xp = (sl.z + 32 * (pick >> 2) + l) * 4 + (pick & 3);
-        const uint16_t t = lid[xj];
-        lid[xj] = lid[xp];
-        lid[xp] = t;
-        const double c = cst_s[sl.x + l + 32 * j];
-        cst_s[sl.x + l + 32 * j] = cst_s[sl.x + l + 32 * pick];
-        cst_s[sl.x + l + 32 * pick] = c;
+      if (pick < 0) {  // one-step augmenting path
+        for (int k = j; k < hi && pick < 0; ++k) {
+          const int b = lid[ix(l, k)] & 15;
+          if ((shared >> b) & 1u) continue;
+          const int o = owner[b];
+          for (int k2 = j + 1; k2 < hi; ++k2) {
+            const uint16_t q2 = lid[ix(o, k2)];
+            if (!((used >> (q2 & 15)) & 1u)) {
+              swap_cols(o, j, k2);  // the owner moves to the free pair
+              used |= 1u << (q2 & 15);
+              word[q2 & 15] = q2;
+              owner[q2 & 15] = (int8_t)o;
+              used &= ~(1u << b);
+              pick = k;
+              break;
+            }
+          }
+        }
       }
-      const uint16_t q = lid[xj];
-      used |= 1u << (q & 15);
-      word[q & 15] = q;
+#ifdef F2M_HEAD_STATS
+      F2M_HEAD_COUNT(j < H ? 4 : 5);
+      if (pick < 0) F2M_HEAD_COUNT(j < H ? 2 : 3);
+#endif
+      if (pick < 0) pick = j;
+      if (pick != j) swap_cols(l, j, pick);
+      const uint16_t q = lid[ix(l, j)];
+      const int b = q & 15;
+      if ((used >> b) & 1u) {
+        shared |= 1u << b;  // a broadcast (or a conflict: the pair stays with its first word)
+      } else {
+        used |= 1u << b;
+        word[b] = q;
+        owner[b] = (int8_t)l;
+      }
     }
   }
 }
@@ -1377,7 +1410,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   if (tid == 0) s_exit = 1;
 #ifdef F2M_HEAD_STATS
   if (tid == 0 && c == 0)
-    printf("head stats: repaired rows %llu\n", g_head_stats[1]);
+    printf("head stats: repaired rows %llu; layout conflicts head %llu / %llu, tail %llu / %llu\n", g_head_stats[1],
+           g_head_stats[2], g_head_stats[4], g_head_stats[3], g_head_stats[5]);
 #endif
 }
 
