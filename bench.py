@@ -32,6 +32,7 @@ partition-resident kernel across ranks, and `clustered_200k_resident`: BASELINE 
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -640,17 +641,22 @@ def run_gpu(args):
         return f2m.full_solve_arrays(xy_pinned.numpy(), k=K, eps=EPS, max_sweeps=MAX_SWEEPS,
                                      out_value=x_host, out_duals=lam_host)
 
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(1, args.warmup)):
         solve_host()
     e2e_times = []
+    rr = None
+    gc.collect()
+    gc.disable()  # as timeit does: no collector pauses inside the timed calls
     barrier()
     for _ in range(args.steps):
+        rr = None  # the previous step's result (device graph, host views) is released outside the timed call
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rr = solve_host()
         e2e_times.append(time.perf_counter() - t0)
     barrier()
+    gc.enable()
     e2e = statistics.mean(e2e_times)
     m = int(rr["graph"].m)
     if ws > 1:
@@ -705,7 +711,9 @@ def run_gpu(args):
         "stage_s": {"knn": r["t_knn"], "duals": r["t_duals"], "extract_verify": r["t_extract"]},
         "roofline": roofline,
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 16 * N_CITIES,
-                "d2h_bytes_per_step": 8 * m + 8 * N_CITIES},
+                "d2h_bytes_per_step": 8 * m + 8 * N_CITIES,
+                "median_s": statistics.median(e2e_times), "min_s": min(e2e_times), "max_s": max(e2e_times),
+                "steps_ms": [round(1e3 * t, 3) for t in e2e_times]},
         "gpu_launches": int(round(launches)),
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
