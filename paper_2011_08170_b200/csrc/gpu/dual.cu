@@ -360,7 +360,11 @@ __global__ void __launch_bounds__(DENSE ? kDenseThreads : kAllPairsThreads, 1) k
 #ifdef F2M_WARP_PROFILE
 constexpr int kProfCtas = 160, kProfWarps = 32, kProfFields = 12;
 __device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
-#define F2M_PROF_T(var) const long long var = clock64()
+// a volatile shared-memory read first: BAR.SYNC.DEFER_BLOCKING lets a warp run on until its next
+// shared-memory access, so without it a clock read after a barrier is taken before the wait
+#define F2M_PROF_T(var) \
+  (void)*(volatile int*)&s_exit; \
+  const long long var = clock64()
 #define F2M_PROF_ADD(f, v) (prof[f] += (unsigned long long)(v))
 #else
 #define F2M_PROF_T(var)
@@ -1138,7 +1142,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
         for (int b = 0; b < kPB; ++b)
           if (base + lane + 64 * b < nh) pend |= 1u << b;
+#ifdef F2M_T_NOHALO  // TIMING ONLY (wrong results): the halo is read without waiting (possibly stale)
+        if (true) {
+#else
         if (s == 0) {
+#endif
           double v[kPB];
 #pragma unroll
           for (int b = 0; b < kPB; ++b)
