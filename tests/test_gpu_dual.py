@@ -94,6 +94,30 @@ def test_sweeps_vs_oracle_b_and_rule(f2m, orc, b, update):
     assert np.array_equal(np.array(st.lam), lam0)
 
 
+@pytest.mark.parametrize("b", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("update", ["midpoint", "paper-difference"])
+def test_head_first_scans_vs_oracle_b_and_rule(f2m, orc, b, update):
+    """The resident kernel's head-first row scans (head of B+2 slots sorted by a network, tail slots
+    compared with the (B+1)-th smallest, rescans + repairs when a tail value enters) and its
+    bank-aware initial slot order, for every list size up to the reference's kMaxB: per-sweep
+    max|delta| and the multipliers after 40 sweeps equal the reference's Jacobi sweeps
+    (dual.cpp:129-167). 60k cities: one lane per boundary row, mostly interior rows."""
+    xy = orc.generate_instance(60000, 900 + b, 1000.0)
+    og = orc.build_knn_graph(xy, 10)
+    g = f2m.build_knn_graph(f2m.Instance.from_points(xy), 10)
+    lam0 = orc.initial_state(og, b=b)
+    st = f2m.make_initial_state(g, b=b)
+    assert np.array_equal(np.array(st.lam), lam0)
+    mx, dv = f2m.jacobi_sweeps(g, st, 40, b=b, update=update, eta=0.7)
+    desc = f2m.last_sweep_kernel_desc()
+    assert "resident" in desc and "two lanes" not in desc, desc
+    for s in range(40):
+        omx, odv = orc.jacobi_sweep(og, lam0, b=b, update=update, eta=0.7)
+        assert mx[s] == omx, s
+    assert dv == odv
+    assert np.array_equal(np.array(st.lam), lam0)
+
+
 def test_gauss_seidel_vs_oracle(f2m, orc):
     xy = orc.generate_instance(300, 5, 100.0)
     og = orc.build_knn_graph(xy, 6)
