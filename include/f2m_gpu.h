@@ -390,6 +390,9 @@ const char* f2m_last_sweep_kernel_desc(void);
  * end-of-sweep barrier, sweeps, interior slices, interior slot columns, boundary slice width).
    Fields 8-10: boundary-row setup, scan, finish + publish. The product build returns F2M_E_ARGUMENT. */
 int f2m_debug_warp_profile(unsigned long long* out, size_t count);
+/* debug builds only (-DF2M_WARP_PROFILE): per-CTA event clocks of 64 sweeps of the last sweep
+   launch, [160][64][4]; reset != 0 zeroes them first. */
+int f2m_debug_sweep_trace(unsigned long long* out, size_t count, int reset);
 /* Algorithmic bytes per sweep of this graph's GDP kernel:
  * 4(n+1) + 2m*(4+8) + 16n. */
 double f2m_sweep_algorithmic_bytes(const f2m_graph* g);

@@ -360,6 +360,16 @@ __global__ void __launch_bounds__(DENSE ? kDenseThreads : kAllPairsThreads, 1) k
 #ifdef F2M_WARP_PROFILE
 constexpr int kProfCtas = 160, kProfWarps = 32, kProfFields = 12;
 __device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
+// per-CTA event clocks (SM clock64, comparable within a CTA) of sweeps [kTraceS0, kTraceS0 + 64):
+// {sweep start, last boundary row published, halo staged (both sync warps), end-of-sweep barrier}
+constexpr int kTraceS0 = 2000, kTraceN = 64;
+__device__ unsigned long long g_strace[kProfCtas][kTraceN][4];
+#define F2M_TRACE_EV(sw, f)                                                                 \
+  do {                                                                                      \
+    const int k_ = (sw) - kTraceS0;                                                         \
+    if (k_ >= 0 && k_ < kTraceN && c < kProfCtas)                                           \
+      atomicMax(&g_strace[c][k_][f], (unsigned long long)clock64());                        \
+  } while (0)
 // a volatile shared-memory read first: BAR.SYNC.DEFER_BLOCKING lets a warp run on until its next
 // shared-memory access, so without it a clock read after a barrier is taken before the wait
 #define F2M_PROF_T(var) \
@@ -369,6 +379,7 @@ __device__ unsigned long long g_wprof[kProfCtas][kProfWarps][kProfFields];
 #else
 #define F2M_PROF_T(var)
 #define F2M_PROF_ADD(f, v)
+#define F2M_TRACE_EV(sw, f)
 #endif
 
 __device__ __forceinline__ void named_sync(int id, int count) {
@@ -1193,6 +1204,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       __syncwarp();
       // hand-off on a hardware barrier (compute warps sleep in bar.sync, no spinning); two ids
       // alternate so the run-ahead arrival for s+1 can never be counted towards sweep s
+      if (lane == 0) F2M_TRACE_EV(s, 2);
       named_arrive(3 + (s & 1), halo_bar);
       if (sw == 0 && lane == 0) s_word = ld_relaxed_u64(&ctl->word);
     }
@@ -1208,6 +1220,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #endif
   for (int s = 0;; ++s) {
     F2M_PROF_T(t0);
+    if (tid == 0) F2M_TRACE_EV(s, 0);
     double* lam = (RES && (s & 1)) ? regB : regA;
     double* lam_next = (s & 1) ? regA : regB;
     const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
@@ -1319,6 +1332,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       }
     }
     F2M_PROF_T(t2);
+    if (lane == 0 && nbnd > 0 && in_halo_bar) F2M_TRACE_EV(s, 1);
     F2M_PROF_ADD(1, t2 - t1);
     // interior slices: one thread per node (throughput-bound phase)
     for (int sl = s_lo + warp; sl < s_int; sl += ncw) {
@@ -1391,6 +1405,12 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       s_stop[s & 1] = (w >> 32) ? (int)(w >> 32) - 1 : -1;
     }
     named_sync(2, cthreads);  // [B]
+#ifdef F2M_WARP_PROFILE
+    if (tid == 0) {
+      (void)*(volatile int*)&s_exit;
+      F2M_TRACE_EV(s, 3);
+    }
+#endif
     F2M_PROF_T(t4);
     F2M_PROF_ADD(3, t4 - t3);
     F2M_PROF_ADD(4, 1);
@@ -2222,6 +2242,28 @@ extern "C" int f2m_debug_warp_profile(unsigned long long* out, size_t count) {
     (void)out;
     (void)count;
     throw Error(F2M_E_ARGUMENT, "warp profile: not a -DF2M_WARP_PROFILE build");
+#endif
+  });
+}
+
+// debug builds only (-DF2M_WARP_PROFILE): per-CTA event clocks of 64 sweeps of the last launch
+// (zeroed first when `reset`), [160 CTAs][64 sweeps][4] = {sweep start, last boundary row
+// published, halo staged, end-of-sweep barrier} (tools/sweep_trace.py)
+extern "C" int f2m_debug_sweep_trace(unsigned long long* out, size_t count, int reset) {
+  return guard([&] {
+#ifdef F2M_WARP_PROFILE
+    if (reset) {
+      static unsigned long long zero[kProfCtas][kTraceN][4];
+      F2M_CUDA(cudaMemcpyToSymbol(g_strace, zero, sizeof(zero)));
+      return;
+    }
+    if (count < (size_t)kProfCtas * kTraceN * 4) throw Error(F2M_E_ARGUMENT, "sweep trace: buffer too small");
+    F2M_CUDA(cudaMemcpyFromSymbol(out, g_strace, sizeof(g_strace)));
+#else
+    (void)out;
+    (void)count;
+    (void)reset;
+    throw Error(F2M_E_ARGUMENT, "sweep trace: not a -DF2M_WARP_PROFILE build");
 #endif
   });
 }

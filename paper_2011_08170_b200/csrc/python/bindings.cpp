@@ -484,6 +484,11 @@ PYBIND11_MODULE(_f2m, m) {
     f2m::check(f2m_debug_warp_profile(out.mutable_data(), static_cast<size_t>(out.size())));
     return out;
   });
+  m.def("debug_sweep_trace", [](bool reset) {
+    py::array_t<unsigned long long> out({160, 64, 4});
+    f2m::check(f2m_debug_sweep_trace(out.mutable_data(), static_cast<size_t>(out.size()), reset ? 1 : 0));
+    return out;
+  }, py::arg("reset") = false);
   m.def("set_allpairs_mode", [](int mode) { f2m::check(f2m_set_allpairs_mode(mode)); }, py::arg("mode"));
   m.def("set_sweep_partition", [](int ctas) { f2m_set_sweep_partition(ctas); }, py::arg("ctas"));
   m.def("set_gpu_list", [](const std::vector<int>& devices) {
