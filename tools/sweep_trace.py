@@ -40,4 +40,13 @@ d = {
     "published_to_barrier": float(np.median((bar - pub)[pub > 0])),
     "barrier_to_next_start": float(np.median((start[:, 1:] - bar[:, :-1])[ok])),
 }
+# per sweep parity (the two-deep-halo form exchanges on even sweeps only)
+for par in (0, 1):
+    sl = slice(par, None, 2)
+    st_, bar_ = start[:, sl], bar[:, sl]
+    nxt = start[:, par + 1::2][:, :st_.shape[1]]
+    m = min(st_.shape[1], nxt.shape[1])
+    ok2 = (st_[:, :m] > 0) & (nxt[:, :m] > 0)
+    d["parity%d_sweep_cycles" % par] = float(np.median((nxt[:, :m] - st_[:, :m])[ok2]))
+    d["parity%d_start_to_barrier" % par] = float(np.median((bar_ - st_)[(st_ > 0) & (bar_ > 0)]))
 print(json.dumps(d))
