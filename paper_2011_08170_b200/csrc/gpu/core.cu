@@ -50,7 +50,6 @@ Topology::~Topology() {
     halo_off.release(); halo.release(); slidx.release();
     cta_int_hi.release(); cta_nint.release(); boff.release(); halo_pub.release();
     sdest.release(); row_nhalo.release();
-    gh_off.release(); gh.release(); gh_h1.release(); gpub.release(); gs_off.release(); gsw.release();
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
@@ -452,85 +451,6 @@ __global__ void k_halo_pub(int64_t h, const int32_t* __restrict__ halo, const in
   pub[i] = boff[c] + (q - lo[c] * 32 - nint[c]);  // q is a boundary node of its owner (symmetric graph)
 }
 
-// ---- two-deep halo (ghost rows)
-__device__ __forceinline__ int cta_of_entry(int G, const int32_t* __restrict__ off, int64_t i) {
-  int a = 0, b = G;  // off[a] <= i < off[a + 1]
-  while (b - a > 1) {
-    const int mid = (a + b) >> 1;
-    if (off[mid] <= i) a = mid; else b = mid;
-  }
-  return a;
-}
-
-// keys (CTA << qbits | position) of H_c: every H1 entry and every out-of-CTA neighbour of an H1
-// row; unused key slots get the sentinel (sorted last)
-__global__ void k_ghost_keys(int64_t h, int G, int n, int max_deg, const int32_t* __restrict__ halo,
-                             const int32_t* __restrict__ halo_off, const int32_t* __restrict__ lo,
-                             const int64_t* __restrict__ sptr, const int32_t* __restrict__ swidth,
-                             const int32_t* __restrict__ scol, const int32_t* __restrict__ seid, int qbits,
-                             uint64_t sentinel, uint64_t* __restrict__ keys) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= h) return;
-  const int c = cta_of_entry(G, halo_off, i);
-  int p0, p1;
-  own_range(c, n, lo, p0, p1);
-  const int q = halo[i];
-  uint64_t* out = keys + i * (int64_t)(1 + max_deg);
-  out[0] = ((uint64_t)(uint32_t)c << qbits) | (uint32_t)q;
-  const int qs = q >> 5, ql = q & 31, w = swidth[qs];
-  for (int j = 0; j < max_deg; ++j) {
-    uint64_t key = sentinel;
-    if (j < w) {
-      const int64_t t = sptr[qs] + 32 * (int64_t)j + ql;
-      const int r = scol[t];
-      if (seid[t] >= 0 && (r < p0 || r >= p1)) key = ((uint64_t)(uint32_t)c << qbits) | (uint32_t)r;
-    }
-    out[1 + j] = key;
-  }
-}
-
-// index in H_c of every H1 entry; the published flag of every H_c position
-__global__ void k_ghost_index(int64_t h, int G, const int32_t* __restrict__ halo, const int32_t* __restrict__ halo_off,
-                              const int32_t* __restrict__ gh, const int32_t* __restrict__ gh_off,
-                              int32_t* __restrict__ gh_h1) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= h) return;
-  const int c = cta_of_entry(G, halo_off, i);
-  const int q = halo[i];
-  int a = gh_off[c], b = gh_off[c + 1];
-  while (a < b) {
-    const int mid = (a + b) >> 1;
-    if (gh[mid] < q) a = mid + 1; else b = mid;
-  }
-  gh_h1[i] = a - gh_off[c];
-}
-__global__ void k_ghost_flag(int64_t hc, const int32_t* __restrict__ gh, int32_t* __restrict__ flag) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < hc) flag[gh[i]] = 1;
-}
-__global__ void k_ghost_pub(int n, const int32_t* __restrict__ flag, const int32_t* __restrict__ idx,
-                            int32_t* __restrict__ gpub) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) gpub[p] = flag[p] ? idx[p] : -1;
-}
-// ghost slices: 32 consecutive H1 rows of a CTA each; width = the widest source SELL slice
-__global__ void k_ghost_slices(int G, const int32_t* __restrict__ halo, const int32_t* __restrict__ halo_off,
-                               const int32_t* __restrict__ gs_off, const int32_t* __restrict__ swidth,
-                               int32_t* __restrict__ gsw) {
-  const int c = blockIdx.x;
-  const int h0 = halo_off[c], h1 = halo_off[c + 1];
-  for (int g = threadIdx.x; g < gs_off[c + 1] - gs_off[c]; g += blockDim.x) {
-    int w = 0;
-    for (int r = h0 + 32 * g; r < min(h1, h0 + 32 * g + 32); ++r) w = max(w, swidth[halo[r] >> 5]);
-    gsw[gs_off[c] + g] = w;
-  }
-}
-__global__ void k_ghost_counts(int G, const int32_t* __restrict__ halo_off, int32_t* __restrict__ cnt) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > G) return;
-  cnt[c] = c < G ? (halo_off[c + 1] - halo_off[c] + 31) / 32 : 0;
-}
-
 // ---------------------------------------------------------------- host helpers
 
 void sort_edges(Topology& t, DBuf<int32_t>& eu, DBuf<int32_t>& ev, DBuf<double>& cost) {
@@ -568,8 +488,6 @@ void identity_perm(Topology& t) {
     launched("iota");
   }
 }
-
-static void build_ghost_topology(Topology& t, size_t limit, int max_slices);
 
 // v2 sweep structures: halo lists, per-slot local indices, CTA adjacency, smem plan.
 static void build_local_index(Topology& t) {
@@ -719,128 +637,6 @@ static void build_local_index(Topology& t) {
   t.resident = resident_bytes <= limit;
   t.smem_bytes = t.resident ? resident_bytes : streaming_bytes;
   F2M_CUDA(cudaStreamSynchronize(s));
-  if (F2M_GHOST && t.resident && t.partition_override == 0 && g_sweep_partition == 0)
-    build_ghost_topology(t, limit, max_slices);
-}
-
-// Two-deep halo for the resident single-GPU sweep (dual.cu GHOST form): H_c, the H1 -> H_c map,
-// the published positions (LL indices) and the ghost-slice widths; sets t.ghost when the ghost
-// layout fits in shared memory. Only the layout: results never depend on it.
-static void build_ghost_topology(Topology& t, size_t limit, int max_slices) {
-  cudaStream_t s = t.stream;
-  const int n = t.n, G = t.sweep_ctas;
-  t.ghost = false;
-  std::vector<int32_t> hoff(G + 1);
-  F2M_CUDA(cudaMemcpyAsync(hoff.data(), t.halo_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
-  const int64_t h = hoff[G];
-  if (h <= 0 || t.max_deg <= 0) return;
-  const int qbits = std::max(bit_width(n - 1), 1);
-  const int key_bits = bit_width(G) + qbits;
-  const uint64_t sentinel = (key_bits >= 64) ? ~0ULL : ((1ull << key_bits) - 1);
-  const int64_t nk = h * (int64_t)(1 + t.max_deg);
-  DBuf<uint64_t> k0(nk, s), k1(nk, s);
-  k_ghost_keys<<<grid_for(h, 128), 128, 0, s>>>(h, G, n, t.max_deg, t.halo.get(), t.halo_off.get(), t.cta_lo.get(),
-                                               t.sptr.get(), t.swidth.get(), t.scol.get(), t.seid.get(), qbits,
-                                               sentinel, k0.get());
-  launched("ghost_keys");
-  DBuf<int64_t> nsel(1, s), hcnt(1, s);
-  {
-    size_t tmp = 0;
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0.get(), k1.get(), nk, 0, key_bits, s));
-    DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k0.get(), k1.get(), nk, 0, key_bits, s));
-    tmp = 0;
-    F2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, k1.get(), k0.get(), nsel.get(), nk, s));
-    DBuf<char> tb2(tmp, s);
-    F2M_CUDA(cub::DeviceSelect::Unique(tb2.get(), tmp, k1.get(), k0.get(), nsel.get(), nk, s));
-    launched("ghost_unique");
-  }
-  k_drop_sentinel<<<1, 1, 0, s>>>(nsel.get(), k0.get(), sentinel, hcnt.get());
-  int64_t hc = 0;
-  F2M_CUDA(cudaMemcpyAsync(pinned_scratch() + 60, hcnt.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
-  hc = pinned_scratch()[60];
-  if (hc <= 0) return;
-  t.gh.alloc(hc, s);
-  t.gh_off.alloc(G + 1, s);
-  {
-    DBuf<int32_t> cnt(G + 1, s);
-    F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (G + 1), s));
-    k_halo_split<<<grid_for(hc, 256), 256, 0, s>>>(hc, k0.get(), qbits, t.gh.get(), cnt.get());
-    size_t tmp = 0;
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.gh_off.get(), G + 1, s));
-    DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.gh_off.get(), G + 1, s));
-  }
-  t.gh_h1.alloc(h, s);
-  k_ghost_index<<<grid_for(h, 256), 256, 0, s>>>(h, G, t.halo.get(), t.halo_off.get(), t.gh.get(), t.gh_off.get(),
-                                                t.gh_h1.get());
-  t.gpub.alloc(n, s);
-  {
-    DBuf<int32_t> flag(n + 1, s), idx(n + 1, s);
-    F2M_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t) * (n + 1), s));
-    k_ghost_flag<<<grid_for(hc, 256), 256, 0, s>>>(hc, t.gh.get(), flag.get());
-    size_t tmp = 0;
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), idx.get(), n + 1, s));
-    DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, flag.get(), idx.get(), n + 1, s));
-    k_ghost_pub<<<grid_for(n, 256), 256, 0, s>>>(n, flag.get(), idx.get(), t.gpub.get());
-    F2M_CUDA(cudaMemcpyAsync(pinned_scratch() + 61, idx.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  }
-  t.gs_off.alloc(G + 1, s);
-  {
-    DBuf<int32_t> cnt(G + 1, s);
-    k_ghost_counts<<<grid_for(G + 1, 128), 128, 0, s>>>(G, t.halo_off.get(), cnt.get());
-    size_t tmp = 0;
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.gs_off.get(), G + 1, s));
-    DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.gs_off.get(), G + 1, s));
-  }
-  std::vector<int32_t> gso(G + 1), gof(G + 1), lo(G + 1);
-  F2M_CUDA(cudaMemcpyAsync(gso.data(), t.gs_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaMemcpyAsync(gof.data(), t.gh_off.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaMemcpyAsync(lo.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
-  t.gnp = reinterpret_cast<const int32_t*>(pinned_scratch() + 61)[0];
-  const int ngs = gso[G];
-  t.gsw.alloc(std::max(ngs, 1), s);
-  k_ghost_slices<<<G, 64, 0, s>>>(G, t.halo.get(), t.halo_off.get(), t.gs_off.get(), t.swidth.get(), t.gsw.get());
-  launched("ghost_slices");
-  std::vector<int32_t> gw(std::max(ngs, 1));
-  F2M_CUDA(cudaMemcpyAsync(gw.data(), t.gsw.get(), sizeof(int32_t) * std::max(ngs, 1), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
-  int max_hc = 0, max_h1 = 0, max_own = 0, max_loc = 0, max_gs = 0;
-  int64_t max_gslots = 0, max_glid4 = 0;
-  for (int c = 0; c < G; ++c) {
-    const int own = std::max(0, std::min(lo[c + 1] * 32, n) - lo[c] * 32);
-    const int hcc = gof[c + 1] - gof[c];
-    max_hc = std::max(max_hc, hcc);
-    max_h1 = std::max(max_h1, hoff[c + 1] - hoff[c]);
-    max_own = std::max(max_own, own);
-    max_loc = std::max(max_loc, own + hcc);
-    max_gs = std::max(max_gs, gso[c + 1] - gso[c]);
-    int64_t sl = 0, l4 = 0;
-    for (int g = gso[c]; g < gso[c + 1]; ++g) {
-      sl += 32 * (int64_t)gw[g];
-      l4 += 32 * (int64_t)((gw[g] + 3) / 4);
-    }
-    max_gslots = std::max(max_gslots, sl);
-    max_glid4 = std::max(max_glid4, l4);
-  }
-  if (max_loc > 65535) return;
-  auto a16 = [](size_t b) { return (b + 15) & ~size_t(15); };
-  t.g_hc_stride = (max_hc + 3) & ~3;
-  t.g_h1_stride = max_h1;
-  t.g_own_stride = max_own;
-  t.g_lam_stride = (int)(a16((size_t)max_loc * sizeof(double)) / sizeof(double));
-  t.g_lid4_stride = t.max_cta_lid4 + max_glid4;
-  const size_t bytes = 2 * (size_t)t.g_lam_stride * sizeof(double) + a16((size_t)t.g_hc_stride * sizeof(int)) +
-                       (size_t)(t.max_cta_slots + max_gslots) * sizeof(double) + (size_t)t.g_lid4_stride * 8 +
-                       a16((size_t)max_own * sizeof(int)) + a16((size_t)max_h1 * sizeof(int)) + 16 +
-                       (size_t)(max_slices + max_gs) * sizeof(int4);
-  t.g_smem_bytes = bytes;
-  t.ghost = bytes <= limit;
 }
 
 void finalize_topology(Topology& t) {

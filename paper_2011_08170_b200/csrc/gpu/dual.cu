@@ -506,19 +506,6 @@ struct Sweep4Args {
   unsigned long long* const* ll_peers;
   unsigned long long* const* cmax_peers;
   const uint32_t* __restrict__ ll_mask;  // [nb] ranks that read each boundary node
-  // two-deep halo (GHOST form, Topology::ghost): H_c positions, H1 -> H_c map, LL index per
-  // position, ghost slices, the global SELL columns / edge ids for the ghost rows' slots
-  const int32_t* __restrict__ gh_off;
-  const int32_t* __restrict__ gh;
-  const int32_t* __restrict__ gh_h1;
-  const int32_t* __restrict__ gpub;
-  const int32_t* __restrict__ gs_off;
-  const int32_t* __restrict__ gsw;
-  const int32_t* __restrict__ scol;
-  const int32_t* __restrict__ seid;
-  int own_stride;
-  int h1_stride;
-  int ghost;
 };
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
@@ -1038,11 +1025,9 @@ __device__ __noinline__ void layout_banks(int B, double* cst_s, ushort4* lid4, i
   }
 }
 
-template <int B, bool RES, int NT, bool PAIR, bool GHOST>
+template <int B, bool RES, int NT, bool PAIR>
 __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
-  static_assert(!GHOST || (RES && !PAIR), "ghost rows: resident form, one lane per boundary row");
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ volatile int s_hstaged;  // GHOST: halo stagings completed (two per exchange sweep)
   __shared__ double red[2][NT / 32];
   __shared__ int s_stop[2];
   __shared__ volatile int s_done;  // sweeps completed by the compute warps
@@ -1087,15 +1072,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   const int h0 = a.halo_off[c], nh = a.halo_off[c + 1] - h0;
   const int64_t slot0 = a.sptr[s_lo];
   const int nslots = (int)(a.sptr[s_hi] - slot0);
-  // GHOST: the halo staged every other sweep is H_c (H1 plus the out-of-CTA neighbours of the H1
-  // rows); the H1 rows are recomputed here as ghost rows (slices appended to the CTA's own)
-  const int g0 = GHOST ? a.gh_off[c] : 0, nhc = GHOST ? a.gh_off[c + 1] - g0 : 0;
-  const int gs0 = GHOST ? a.gs_off[c] : 0, ngs = GHOST ? a.gs_off[c + 1] - gs0 : 0;
-  int ngslots = 0;
-  if (GHOST)
-    for (int g = 0; g < ngs; ++g) ngslots += 32 * a.gsw[gs0 + g];
-  const int nstage = GHOST ? nhc : nh;                                    // halo entries staged
-  const int32_t* __restrict__ stage_pos = GHOST ? a.gh + g0 : a.halo + h0;  // their positions
   double* regA = reinterpret_cast<double*>(smem);
   double* regB = regA + (RES ? a.lam_stride : 0);
   int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
@@ -1103,19 +1079,16 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // resident local indices, packed 4 slots per lane: slice t's slot (j, lane) is component j % 4 of
   // lid4[slc[t].z + 32 (j / 4) + lane] — one 8-byte load per lane per 4 slots instead of four 2-byte
   // loads (widths are padded to a multiple of 4 for this array only; the padding is never read)
-  ushort4* lid4 = reinterpret_cast<ushort4*>(cst_s + (RES ? nslots + ngslots : 0));
+  ushort4* lid4 = reinterpret_cast<ushort4*>(cst_s + (RES ? nslots : 0));
   const int nlid4 = RES ? a.lid4_stride : 0;
-  int* rowll = reinterpret_cast<int*>(lid4 + nlid4);         // GHOST: LL index of each own row (-1: none)
-  int* gdst = rowll + (GHOST ? a.own_stride : 0);             // GHOST: local index of each ghost row's node
   // per-slice {slot offset, width, packed-index offset} of this CTA: no global loads on the sweep
   // path. The 16-byte alignment is computed on the offset from `smem` so the compiler keeps the
   // shared address space (a uintptr_t round trip turned these into generic LD.E loads)
-  const size_t slc_off = ((size_t)(reinterpret_cast<unsigned char*>(gdst + (GHOST ? a.h1_stride : 0)) - smem) + 15) &
-                         ~size_t(15);
+  const size_t slc_off = ((size_t)(reinterpret_cast<unsigned char*>(lid4 + nlid4) - smem) + 15) & ~size_t(15);
   int4* slc = reinterpret_cast<int4*>(smem + slc_off);
   const double* __restrict__ gcost = a.scost + slot0;
   const uint16_t* __restrict__ glid = a.slidx + slot0;
-  for (int i = tid; i < nstage; i += blockDim.x) halo_s[i] = GHOST ? a.gpub[stage_pos[i]] : a.halo_pub[h0 + i];
+  for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
   if (tid == 0) {  // <= ~60 slices per CTA in the resident regime
     int z = 0;
     for (int i = 0; i < s_hi - s_lo; ++i) {
@@ -1123,16 +1096,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       slc[i] = make_int4((int)(a.sptr[s_lo + i] - slot0), w, z, 0);
       z += 32 * ((w + 3) >> 2);
     }
-    if (GHOST) {  // ghost slices after the own ones: slots from nslots on, packed indices from z on
-      int gz = nslots;
-      for (int g = 0; g < ngs; ++g) {
-        const int w = a.gsw[gs0 + g];
-        slc[s_hi - s_lo + g] = make_int4(gz, w, z, 0);
-        gz += 32 * w;
-        z += 32 * ((w + 3) >> 2);
-      }
-    }
-    s_hstaged = 0;
   }
   if (RES) {
     __syncthreads();  // slice table in place
@@ -1146,68 +1109,20 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         if (slc[mid].x <= d) t0 = mid; else t1 = mid;
       }
       const int r = d - slc[t0].x, j = r >> 5;
-      int li = glid[i];
-      if (GHOST && li >= own) li = own + a.gh_h1[h0 + li - own];  // H1 entry -> its H_c entry
-      reinterpret_cast<uint16_t*>(lid4)[(size_t)(slc[t0].z + 32 * (j >> 2) + (r & 31)) * 4 + (j & 3)] = (uint16_t)li;
-    }
-    if (GHOST) {
-      // ghost rows: the H1 rows' SELL slots (graph.cpp incident order does not matter), each
-      // neighbour mapped to its local index (own, or its H_c entry); padding +inf on the node itself
-      for (int r = tid; r < 32 * ngs; r += blockDim.x) {
-        const int4 gsl = slc[s_hi - s_lo + (r >> 5)];
-        const int ln = r & 31;
-        const bool real = r < nh;
-        const int q = real ? a.halo[h0 + r] : 0;
-        const int self = real ? own + a.gh_h1[h0 + r] : 0;
-        if (real) gdst[r] = self;
-        const int qs = q >> 5, ql = q & 31, wq = real ? a.swidth[qs] : 0;
-        const int64_t qb = real ? a.sptr[qs] : 0;
-        for (int j = 0; j < gsl.y; ++j) {
-          double cv = CUDART_INF;
-          int li = self;
-          if (j < wq) {
-            const int64_t t = qb + 32 * (int64_t)j + ql;
-            if (a.seid[t] >= 0) {
-              cv = a.scost[t];
-              const int rp = a.scol[t];
-              if (rp >= p0 && rp < p0 + own) {
-                li = rp - p0;
-              } else {
-                int lo2 = 0, hi2 = nhc;
-                while (lo2 < hi2) {
-                  const int mid = (lo2 + hi2) >> 1;
-                  if (stage_pos[mid] < rp) lo2 = mid + 1; else hi2 = mid;
-                }
-                li = own + lo2;
-              }
-            }
-          }
-          cst_s[gsl.x + ln + 32 * j] = cv;
-          reinterpret_cast<uint16_t*>(lid4)[(size_t)(gsl.z + 32 * (j >> 2) + ln) * 4 + (j & 3)] = (uint16_t)li;
-        }
-      }
-      for (int i = tid; i < own; i += blockDim.x) rowll[i] = a.gpub[p0 + i];
+      reinterpret_cast<uint16_t*>(lid4)[(size_t)(slc[t0].z + 32 * (j >> 2) + (r & 31)) * 4 + (j & 3)] = glid[i];
     }
     for (int i = tid; i < own; i += blockDim.x) regA[i] = a.gl[p0 + i];
     if (kHead && F2M_BANK_LAYOUT) {
       // initial slot order: heads at the initial multipliers (halo staged here once), then
       // bank-aware columns
-      for (int i = tid; i < nstage; i += blockDim.x) regA[own + i] = __ldcg(a.gl + stage_pos[i]);
+      for (int i = tid; i < nh; i += blockDim.x) regA[own + i] = __ldcg(a.gl + a.halo[h0 + i]);
       __syncthreads();
       for (int lp = tid; lp < own; lp += blockDim.x) layout_head(B, cst_s, lid4, slc[lp >> 5], lp & 31, regA[lp], regA);
-      if (GHOST)
-        for (int r = tid; r < nh; r += blockDim.x)
-          layout_head(B, cst_s, lid4, slc[ns + (r >> 5)], r & 31, regA[gdst[r]], regA);
       __syncthreads();
       for (int hs = tid; hs < 2 * ns; hs += blockDim.x) {  // one thread per half-slice
         const int l0 = 16 * (hs & 1), nrows = min(16, own - 32 * (hs >> 1) - l0);
         if (nrows > 0) layout_banks(B, cst_s, lid4, slc[hs >> 1], l0, nrows);
       }
-      if (GHOST)
-        for (int hs = tid; hs < 2 * ngs; hs += blockDim.x) {
-          const int l0 = 16 * (hs & 1), nrows = min(16, nh - 32 * (hs >> 1) - l0);
-          if (nrows > 0) layout_banks(B, cst_s, lid4, slc[ns + (hs >> 1)], l0, nrows);
-        }
     }
   }
   if (tid == 0) {
@@ -1225,7 +1140,6 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     // 64-register budget (1024 threads) may favour fewer loads in flight
     constexpr int kPB = RES ? 8 : F2M_STREAM_POLL;
     for (int s = 0;; ++s) {
-      if (GHOST && (s & 1)) continue;  // the odd sweeps read ghost rows: no exchange
       const int need = (RES && a.runahead) ? s - 1 : s;  // the region being filled is no longer read
       while (s_done < need && !s_exit) __nanosleep(32);
       if (s_exit) break;
@@ -1234,11 +1148,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
       const uint64_t t0 = globaltimer_ns();
       bool quit = false;
-      for (int base = sw * 32; base < nstage && !quit; base += 64 * kPB) {
+      for (int base = sw * 32; base < nh && !quit; base += 64 * kPB) {
         unsigned pend = 0;
 #pragma unroll
         for (int b = 0; b < kPB; ++b)
-          if (base + lane + 64 * b < nstage) pend |= 1u << b;
+          if (base + lane + 64 * b < nh) pend |= 1u << b;
 #ifdef F2M_T_NOHALO  // TIMING ONLY (wrong results): the halo is read without waiting (possibly stale)
         if (true) {
 #else
@@ -1247,7 +1161,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           double v[kPB];
 #pragma unroll
           for (int b = 0; b < kPB; ++b)
-            if (pend & (1u << b)) v[b] = __ldcg(gin + stage_pos[base + lane + 64 * b]);
+            if (pend & (1u << b)) v[b] = __ldcg(gin + a.halo[h0 + base + lane + 64 * b]);
 #pragma unroll
           for (int b = 0; b < kPB; ++b)
             if (pend & (1u << b)) lam[own + base + lane + 64 * b] = v[b];
@@ -1291,11 +1205,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       // hand-off on a hardware barrier (compute warps sleep in bar.sync, no spinning); two ids
       // alternate so the run-ahead arrival for s+1 can never be counted towards sweep s
       if (lane == 0) F2M_TRACE_EV(s, 2);
-      named_arrive(3 + (GHOST ? ((s >> 1) & 1) : (s & 1)), halo_bar);
-      if (GHOST && lane == 0) {  // the ghost-row warps wait on this count, not on the barrier
-        __threadfence_block();
-        atomicAdd(const_cast<int*>(&s_hstaged), 1);
-      }
+      named_arrive(3 + (s & 1), halo_bar);
       if (sw == 0 && lane == 0) s_word = ld_relaxed_u64(&ctl->word);
     }
     return;
@@ -1320,10 +1230,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       named_sync(2, cthreads);
     }
     double mx = 0.0;
-    // GHOST: even sweeps exchange (their boundary rows wait for H_c), odd sweeps read the ghost
-    // rows' results and publish every row some other CTA's H_c holds
-    const bool xs = !GHOST || !(s & 1);
-    if (in_halo_bar && xs) named_sync(3 + (GHOST ? ((s >> 1) & 1) : (s & 1)), halo_bar);  // halo of sweep s staged
+    if (in_halo_bar) named_sync(3 + (s & 1), halo_bar);  // halo of sweep s staged
     F2M_PROF_T(t1);
     F2M_PROF_ADD(0, t1 - t0);
     unsigned long long* llout = a.ll + (size_t)((s + 1) % kLLRing) * a.nb * 2;
@@ -1412,11 +1319,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           F2M_PROF_T(tb);
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
-          if (GHOST) {
-            if (!xs && rowll[lp] >= 0) st_ll(llout + 2 * rowll[lp], nl, (unsigned)s + 1);
-          } else if (lp >= nint) {
-            publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
-          }
+          if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
           gout[p] = nl;
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
@@ -1466,48 +1369,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       }
       const double d = delta_of<B>(sv, a.update);
       const double nl = dadd(lv, dmul(a.eta, d));
-      if (GHOST && !xs && rowll[lp] >= 0) st_ll(llout + 2 * rowll[lp], nl, (unsigned)s + 1);
       gout[p] = nl;
       if (RES) lam_next[lp] = nl;
       const double ad = fabs(d);
       mx = mx < ad ? ad : mx;
-    }
-    if (GHOST && xs) {
-      // ghost rows (the H1 nodes' rows, recomputed here: their multipliers of sweep s+1 for the odd
-      // sweep's boundary rows), on the warps without boundary rows, after their interior slice
-      const int rw = brow >> 5, nbw = (bthreads + 31) / 32;
-      const int gstride = ncw > nbw ? ncw - nbw : ncw, gfirst = ncw > nbw ? rw - nbw : rw;
-      if (gfirst >= 0) {
-        for (int g = gfirst; g < ngs; g += gstride) {
-          const int target = 2 * ((s >> 1) + 1);
-          while (s_hstaged < target) __nanosleep(16);
-          __threadfence_block();
-          const int r = 32 * g + lane;
-          if (r >= nh) continue;
-          const int4 sw2 = slc[s_hi - s_lo + g];
-          const int lb = sw2.x + lane;
-          const int w = sw2.y;
-          const int node = gdst[r];
-          const double lv = lam[node];
-          double sv[B + 1];
-#pragma unroll
-          for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-          if (w > B + 1) {
-            double hv[B + 2];
-            if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w)) {
-#pragma unroll
-              for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
-              row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
-              row_repair<B + 1>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w);
-            }
-#pragma unroll
-            for (int i = 0; i <= B; ++i) sv[i] = hv[i];
-          } else {
-            row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
-          }
-          lam_next[node] = dadd(lv, dmul(a.eta, delta_of<B>(sv, a.update)));
-        }
-      }
     }
     F2M_PROF_T(t3);
     F2M_PROF_ADD(2, t3 - t2);
@@ -1578,9 +1443,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #endif
 }
 
-template <int B, bool RES, int NT, bool PAIR, bool GHOST>
+template <int B, bool RES, int NT, bool PAIR>
 static void launch_sweep5(const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
-  auto fn = k_gdp_sweep5<B, RES, NT, PAIR, GHOST>;
+  auto fn = k_gdp_sweep5<B, RES, NT, PAIR>;
   F2M_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&a, (void*)&ctl};
   F2M_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(NT), args, smem, s));
@@ -1604,17 +1469,17 @@ constexpr int kStreamingThreads = F2M_STREAMING_THREADS;
 // 3.66 (1024) — more warps hide more latency until ptxas' register budget (65536 / threads)
 // serialises each row's load chain (640 was best with the interior-first order). The streaming
 // layout keeps 1024 threads for memory-level parallelism.
-template <bool RES, int NT, bool PAIR, bool GHOST = false>
+template <bool RES, int NT, bool PAIR>
 static void dispatch_sweep5_b(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, size_t smem, cudaStream_t s) {
   switch (b) {
-    case 1: launch_sweep5<1, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    case 2: launch_sweep5<2, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    case 3: launch_sweep5<3, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    case 4: launch_sweep5<4, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    case 5: launch_sweep5<5, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    case 6: launch_sweep5<6, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    case 7: launch_sweep5<7, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
-    default: launch_sweep5<8, RES, NT, PAIR, GHOST>(a, ctl, ctas, smem, s); break;
+    case 1: launch_sweep5<1, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 2: launch_sweep5<2, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 3: launch_sweep5<3, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 4: launch_sweep5<4, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 5: launch_sweep5<5, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 6: launch_sweep5<6, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    case 7: launch_sweep5<7, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
+    default: launch_sweep5<8, RES, NT, PAIR>(a, ctl, ctas, smem, s); break;
   }
 }
 
@@ -1622,7 +1487,6 @@ static void dispatch_sweep5_b(int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ct
 // one thread per boundary row, streaming (slots read from global memory every sweep)
 static void dispatch_sweep5(const Topology& t, int b, const Sweep4Args& a, Sweep4Ctl* ctl, int ctas, cudaStream_t s) {
   if (t.resident && a.pair_rows) dispatch_sweep5_b<true, kResidentThreads, true>(b, a, ctl, ctas, t.smem_bytes, s);
-  else if (t.resident && a.ghost) dispatch_sweep5_b<true, kResidentThreads, false, true>(b, a, ctl, ctas, t.g_smem_bytes, s);
   else if (t.resident) dispatch_sweep5_b<true, kResidentThreads, false>(b, a, ctl, ctas, t.smem_bytes, s);
   else dispatch_sweep5_b<false, kStreamingThreads, false>(b, a, ctl, ctas, t.smem_bytes, s);
 }
@@ -1779,9 +1643,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     const int G = t.sweep_ctas;
     DBuf<double> ring((size_t)kLamBufs * std::max(t.n, 1), s);
     DBuf<Sweep4Ctl> ctl(1, s);
-    // two-deep halo when built and the graph is not in the two-lanes-per-boundary-row regime
-    const bool ghost = t.ghost && !(t.n <= kPairRowsPerCta * G) && F2M_HEAD_SCAN;
-    const int nb = std::max(ghost ? t.gnp : t.nboundary, 1);
+    const int nb = std::max(t.nboundary, 1);
     DBuf<unsigned long long> ll((size_t)kLLRing * nb * 2, s);
     DBuf<unsigned long long> cmax((size_t)kCmaxRing * G * 2, s);
     // tags restart at 1 every launch: stale words from an earlier launch must not match
@@ -1828,22 +1690,6 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
     a.halo_stride = (t.max_halo + 3) & ~3;
     a.lid4_stride = (int)t.max_cta_lid4;
-    a.ghost = ghost ? 1 : 0;
-    a.gh_off = t.gh_off.get();
-    a.gh = t.gh.get();
-    a.gh_h1 = t.gh_h1.get();
-    a.gpub = t.gpub.get();
-    a.gs_off = t.gs_off.get();
-    a.gsw = t.gsw.get();
-    a.scol = t.scol.get();
-    a.seid = t.seid.get();
-    a.own_stride = t.g_own_stride;
-    a.h1_stride = t.g_h1_stride;
-    if (ghost) {
-      a.lam_stride = t.g_lam_stride;
-      a.halo_stride = t.g_hc_stride;
-      a.lid4_stride = (int)t.g_lid4_stride;
-    }
     a.cta_base = 0;
     a.g_total = G;
     a.npeers = 0;
@@ -1858,7 +1704,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
                           "> (persistent: " + std::to_string(G) +
                           " partition CTAs + 1 convergence-master CTA, LL halo exchange, " +
                           std::to_string(t.smem_bytes) + " B smem/CTA" +
-                          (a.pair_rows ? ", two lanes per boundary row)" : ghost ? ", two-deep halo: exchange every other sweep)" : ")");
+                          (a.pair_rows ? ", two lanes per boundary row)" : ")");
       dispatch_sweep5(t, cfg.b, a, ctl.get(), G + 1, s);
       launched("gdp_sweep5");
     }
@@ -2554,7 +2400,6 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.approx_sum = g->approx_sum.get();
     a.mean_out = nullptr;
     a.pair_rows = t.n <= kPairRowsPerCta * G ? 1 : 0;
-    a.ghost = 0;  // the two-deep halo is a single-GPU form
     a.cmax = d_cmax;
     a.eta = cfg->eta;
     a.update = cfg->update;

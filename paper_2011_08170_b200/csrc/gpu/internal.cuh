@@ -113,10 +113,6 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
-#ifndef F2M_GHOST
-#define F2M_GHOST 0  // two-deep halo (ghost rows): measured slower (profiles/r02_ncu_sweep.md), off
-#endif
-
 // ---------------------------------------------------------------- graph structures
 struct Topology {
   int dev = 0;
@@ -164,23 +160,6 @@ struct Topology {
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
   int64_t max_cta_lid4 = 0;    // max over CTAs of packed local-index entries (ushort4, widths padded to 4)
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
-  // two-deep halo (ghost rows; dual.cu k_gdp_sweep5<..., GHOST>): per CTA the halo H_c = the
-  // out-of-CTA neighbours of its rows (H1, the existing halo list) and of the H1 rows, sorted;
-  // the H1 rows are recomputed locally ("ghost rows"), so the exchange happens every other sweep
-  bool ghost = false;          // built, and the ghost layout fits in shared memory
-  DBuf<int32_t> gh_off;        // [ctas+1]
-  DBuf<int32_t> gh;            // positions of H_c, sorted per CTA
-  DBuf<int32_t> gh_h1;         // [halo entries] index in H_c of each H1 entry
-  DBuf<int32_t> gpub;          // [n] LL index of each position that some other CTA's H_c holds, else -1
-  DBuf<int32_t> gs_off;        // [ctas+1] ghost slices (32 H1 rows each) per CTA, prefix
-  DBuf<int32_t> gsw;           // [ghost slices] width (widest source SELL slice of its rows)
-  int gnp = 0;                 // published positions (LL entries per ring slot)
-  int g_hc_stride = 0;         // max |H_c| (multiple of 4)
-  int g_h1_stride = 0;         // max |H1_c|
-  int g_own_stride = 0;        // max own rows per CTA
-  int g_lam_stride = 0;        // doubles per multiplier region: max (own + |H_c|), 16-byte aligned
-  int64_t g_lid4_stride = 0;   // max own + ghost packed-index entries
-  size_t g_smem_bytes = 0;
   int partition_override = 0;  // > 0: partition CTA count for finalize_topology (multi-GPU replicas)
   ~Topology();
 };
