@@ -787,16 +787,6 @@ __device__ __forceinline__ void row_scan(double (&sv)[B + 1], double lv, const d
 #ifndef F2M_BANK_LAYOUT
 #define F2M_BANK_LAYOUT 1  // bank-aware initial slot order of the resident rows (layout_banks)
 #endif
-#ifdef F2M_T_CF  // TIMING ONLY (wrong results): bank-conflict-free multiplier gathers in the head scans
-#define F2M_LIDX(q_) (((q_) & ~15) | (threadIdx.x & 15))
-#else
-#define F2M_LIDX(q_) (q_)
-#endif
-#ifdef F2M_HEAD_TIMING_NORESCAN  // TIMING ONLY (wrong results): the rescan path compiled but never taken
-#define F2M_HEAD_NORESCAN && a.poll_ns == 0xdeadbeefu
-#else
-#define F2M_HEAD_NORESCAN
-#endif
 #ifdef F2M_HEAD_STATS  // debug build: repaired rows, printed at exit
 __device__ unsigned long long g_head_stats[8];
 #define F2M_HEAD_COUNT(i) atomicAdd(&g_head_stats[i], 1ull)
@@ -833,7 +823,7 @@ __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, co
     li[4 * g + 3] = q.w;
   }
 #pragma unroll
-  for (int h = 0; h < H; ++h) sv[h] = dsub(dsub(cst_s[lb + 32 * h], lv), lam[F2M_LIDX(li[h])]);
+  for (int h = 0; h < H; ++h) sv[h] = dsub(dsub(cst_s[lb + 32 * h], lv), lam[li[h]]);
   auto cas = [&](int i, int k) {
     const bool sw = sv[k] < sv[i];
     const double lo = sw ? sv[k] : sv[i];
@@ -856,14 +846,7 @@ __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, co
   const double thr = sv[B];
   bool hit = false;
   int j = H;
-#ifdef F2M_TIMING_F32TAIL  // TIMING ONLY (wrong results): tail compares on 4-byte costs / multipliers
-  const float* c32 = reinterpret_cast<const float*>(cst_s);
-  const float* l32 = reinterpret_cast<const float*>(lam);
-  const float lv32 = (float)lv, thr32 = (float)thr;
-#define F2M_TAILV(jj, idx) (__fsub_rn(__fsub_rn(c32[lb + 32 * (jj)], lv32), l32[idx]) < thr32)
-#else
-#define F2M_TAILV(jj, idx) (dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[F2M_LIDX(idx)]) < thr)
-#endif
+#define F2M_TAILV(jj, idx) (dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[idx]) < thr)
   if (H % 4) {  // tail slots of the last head group
 #pragma unroll
     for (int u = 0; u < (4 - H % 4) % 4; ++u)
@@ -1153,11 +1136,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
         for (int b = 0; b < kPB; ++b)
           if (base + lane + 64 * b < nh) pend |= 1u << b;
-#ifdef F2M_T_NOHALO  // TIMING ONLY (wrong results): the halo is read without waiting (possibly stale)
-        if (true) {
-#else
         if (s == 0) {
-#endif
           double v[kPB];
 #pragma unroll
           for (int b = 0; b < kPB; ++b)
@@ -1305,7 +1284,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           // one width, so the interior rows' batches apply without predication
           if (kHead && w > B + 1) {
             double hv[B + 2];
-            if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), lb, w) F2M_HEAD_NORESCAN) {
+            if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), lb, w)) {
 #pragma unroll
               for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
               row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
@@ -1356,7 +1335,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
       if (kHead && w > B + 1) {
         double hv[B + 2];
-        if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w) F2M_HEAD_NORESCAN) {
+        if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w)) {
 #pragma unroll
           for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
           row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
