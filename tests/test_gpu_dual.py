@@ -118,6 +118,29 @@ def test_head_first_scans_vs_oracle_b_and_rule(f2m, orc, b, update):
     assert np.array_equal(np.array(st.lam), lam0)
 
 
+@pytest.mark.parametrize("k,rounded", [(24, False), (40, True)])
+def test_head_first_scans_wide_rows(f2m, orc, k, rounded):
+    """Wide rows (k = 24 / 40: slice widths past 32, many packed-index groups per row, integer
+    costs with exact ties when rounded) through the head-first scans, repairs and the bank-aware
+    layout: per-sweep max|delta| and the multipliers equal the reference's Jacobi sweeps."""
+    xy = orc.generate_instance(50000, 77 + k, 1000.0)
+    og = orc.build_knn_graph(xy, k, rounded=rounded)
+    inst = f2m.Instance.from_points(xy)
+    if rounded:
+        inst.mode = f2m.DistanceMode.EUC2D_ROUNDED
+    g = f2m.build_knn_graph(inst, k)
+    lam0 = orc.initial_state(og)
+    st = f2m.make_initial_state(g)
+    assert np.array_equal(np.array(st.lam), lam0)
+    mx, dv = f2m.jacobi_sweeps(g, st, 25)
+    assert "resident" in f2m.last_sweep_kernel_desc()
+    for s in range(25):
+        omx, odv = orc.jacobi_sweep(og, lam0)
+        assert mx[s] == omx, s
+    assert dv == odv
+    assert np.array_equal(np.array(st.lam), lam0)
+
+
 def test_gauss_seidel_vs_oracle(f2m, orc):
     xy = orc.generate_instance(300, 5, 100.0)
     og = orc.build_knn_graph(xy, 6)
