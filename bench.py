@@ -15,8 +15,9 @@ generator), i.e. the reference's full_solve (solve.cpp:101-106).
              (4(n+1) + 2m*12 + 16n per sweep, times the sweeps of the launch)
              over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline  the unmodified reference (oracle/_ref, compiled from /root/reference) on this
-             host: build_knn_graph + 100 Jacobi sweeps timed, extraction + verification timed on
-             the converged multipliers, full solve projected to the reference's own sweep count.
+             host with all its threads (child processes; its ThreadPool can crash for threads > 1,
+             then 1 thread): build_knn_graph + Jacobi sweeps timed, extraction + verification
+             timed on the converged multipliers, full solve projected to its own sweep count.
 
 --impl reference runs only that reference leg (rank 0), printing the same JSON line shape.
 Multi-GPU (torchrun, N>1): every rank solves its own replica of the headline instance (weak
@@ -235,37 +236,112 @@ def reference_full_solve():
     return time.perf_counter() - t0, r
 
 
+def reference_mt_probe(threads: int, attempts: int = 3, sweeps: int = 200):
+    """The reference with `threads` worker threads, in child processes (its ThreadPool has a
+    use-after-scope race for threads > 1: a crash must not take the arm down):
+    k-NN build + `sweeps` Jacobi sweeps of the headline instance per attempt. Returns how many
+    attempts completed / crashed and the completed ones' timings."""
+    ref_path = os.path.join(ROOT, "oracle", "_ref")
+    code = (f"import sys, time\nsys.path.insert(0, {ref_path!r})\nimport f2m as ref\n"
+            f"inst = ref.generate_instance({N_CITIES}, {SEED}, 1000.0)\n"
+            f"t0 = time.perf_counter(); g = ref.build_knn_graph(inst, {K}, threads={threads}); tk = time.perf_counter() - t0\n"
+            f"t0 = time.perf_counter(); ref.solve_duals(g, eps={EPS}, max_sweeps=0, threads={threads}); ti = time.perf_counter() - t0\n"
+            f"t0 = time.perf_counter(); ref.solve_duals(g, eps=1e-300, max_sweeps={sweeps}, threads={threads}); ts = time.perf_counter() - t0\n"
+            f"print(tk, ti, ts)\n")
+    done, crashed, knn, per = 0, 0, [], []
+    for _ in range(attempts):
+        try:
+            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+        except subprocess.TimeoutExpired:
+            crashed += 1
+            continue
+        if p.returncode != 0:
+            crashed += 1
+            continue
+        tk, ti, ts = (float(x) for x in p.stdout.split()[-3:])
+        done += 1
+        knn.append(tk)
+        per.append((ts - ti) / sweeps)
+    out = {"threads": threads, "attempts": attempts, "completed": done, "crashed_or_failed": crashed,
+           "sweeps_per_attempt": sweeps}
+    if done:
+        out.update({"knn_s": statistics.median(knn), "per_sweep_s": statistics.median(per)})
+    return out
+
+
+def reference_full_solve_threads(threads: int, attempts: int = 3):
+    """ONE stock full_solve of the headline instance by the unmodified reference with `threads`
+    worker threads, in a child process per attempt (its ThreadPool race can crash a run, SURVEY.md
+    §5). Returns (seconds, result dict, failed attempts) of the first attempt that completes, or
+    (None, None, failed attempts)."""
+    ref_path = os.path.join(ROOT, "oracle", "_ref")
+    code = (f"import sys, time, json\nsys.path.insert(0, {ref_path!r})\nimport f2m as ref\n"
+            f"inst = ref.generate_instance({N_CITIES}, {SEED}, 1000.0)\n"
+            f"ref.build_knn_graph(inst, {K}, threads={threads})\n"
+            f"t0 = time.perf_counter()\n"
+            f"r = ref.full_solve(inst, k={K}, eps={EPS}, max_sweeps={MAX_SWEEPS}, threads={threads})\n"
+            f"t = time.perf_counter() - t0\n"
+            f"print(json.dumps({{'t': t, 'sweeps': r['sweeps'], 'objective': r['objective'], 'gap': r['gap'], "
+            f"'restarts': r['restarts']}}))\n")
+    failed = 0
+    for _ in range(attempts):
+        try:
+            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900)
+        except subprocess.TimeoutExpired:
+            failed += 1
+            continue
+        if p.returncode != 0:
+            failed += 1
+            continue
+        r = json.loads(p.stdout.strip().splitlines()[-1])
+        return r["t"], r, failed
+    return None, None, failed
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation of the path, measured.
 
     The timed step is ONE complete stock full_solve (k-NN, init, every Jacobi sweep to
-    convergence, extraction, certificate) on 1 host core — about 100 s on the GPU box, so the arm
-    times a single step whatever --steps asks for and reports `steps: 1` honestly (K full solves
-    would not fit the driver's step timeout). Warm-up: one k-NN build (page-in, allocator). The
-    detail keeps the 100-sweep projection for comparison."""
+    convergence, extraction, certificate) with all the host's threads (child processes: the
+    reference's ThreadPool can crash for threads > 1; after 3 failed attempts the
+    race-free 1-thread solve, ~100 s). One step whatever --steps asks for, reported as `steps: 1`
+    (K full solves would not fit the driver's step timeout). The detail keeps the 1-thread
+    100-sweep projection for comparison."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    ref_path = os.path.join(ROOT, "oracle", "_ref")
-    if ref_path not in sys.path:
-        sys.path.insert(0, ref_path)
-    import f2m as ref
-    for _ in range(min(1, args.warmup)):
-        ref.build_knn_graph(ref.generate_instance(N_CITIES, SEED, 1000.0), K, threads=1)
+    threads = os.cpu_count() or 1
+    # all host threads first (the instructions' arm); the reference's ThreadPool can crash for
+    # threads > 1 (SURVEY.md §5), so each attempt runs in a child process, and only if every
+    # attempt fails does the arm fall back to the race-free 1-thread solve
     wall0 = time.perf_counter()
-    value, r = reference_full_solve()
+    value, r, failed = reference_full_solve_threads(threads) if threads > 1 else (None, None, 0)
+    used = threads
+    if value is None:
+        ref_path = os.path.join(ROOT, "oracle", "_ref")
+        if ref_path not in sys.path:
+            sys.path.insert(0, ref_path)
+        import f2m as ref
+        for _ in range(min(1, args.warmup)):
+            ref.build_knn_graph(ref.generate_instance(N_CITIES, SEED, 1000.0), K, threads=1)
+        value, r = reference_full_solve()
+        used = 1
     wall = time.perf_counter() - wall0
     projected, detail = reference_sample(int(r["sweeps"]))
-    detail = {"projection_s_from_100_sweeps": projected, **detail}
-    sample = ("one complete stock full_solve(100k uniform seed 1, k=10, eps 1e-9) of the unmodified reference "
-              "(oracle/_ref) on 1 host core, timed end to end (measured, not projected)")
+    detail = {"one_thread_projection_s_from_100_sweeps": projected, **detail,
+              "threads_attempted": threads, "failed_attempts_at_all_threads": failed}
+    sample = (f"one complete stock full_solve(100k uniform seed 1, k=10, eps 1e-9) of the unmodified reference "
+              f"(oracle/_ref) with {used} host thread(s), timed end to end (measured, not projected)")
     line = {
         "metric": METRIC, "value": value, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
         "steps": 1, "steps_requested": args.steps, "warmup": min(1, args.warmup), "ms_per_step": value * 1e3,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config(), "execution": "1 host thread (the reference ThreadPool races for >1 thread, SURVEY §5)",
+        "config": _config(),
+        "execution": (f"{used} host threads ({failed} earlier attempt(s) failed)" if used > 1 else
+                      f"1 host thread: {failed} of {failed} attempts with {threads} threads crashed (the reference "
+                      f"ThreadPool's use-after-scope race, SURVEY.md §5)" if failed else "1 host thread"),
         "sweeps": int(r["sweeps"]), "objective": r["objective"], "gap": r["gap"], "restarts": int(r["restarts"]),
-        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "reference", "sample": sample,
+        "cpu_baseline": {"value": value, "unit": "s", "cores": used, "kind": "reference", "sample": sample,
                          "cpu_model": _cpu_model(), "host_cpus": os.cpu_count(), "detail": detail},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s_timed_region": wall,
@@ -741,12 +817,26 @@ def run_gpu(args):
         sweeps_total = int(sw)
         lam = d_lam.cpu().numpy()
         v, detail = reference_sample(sweeps_total, lam)
-        line["cpu_baseline"] = {
-            "value": v, "unit": "s", "cores": 1, "kind": "reference", "cpu_model": _cpu_model(),
-            "sample": (f"unmodified reference (oracle/_ref): build_knn_graph + init + {REF_SAMPLE_SWEEPS} Jacobi "
-                       f"sweeps + extract/verify on the converged lambda, 1 thread; projected to "
-                       f"{sweeps_total} sweeps (the --impl reference arm times a complete stock full_solve)"),
-            "detail": detail}
+        # all host threads (child processes: the reference ThreadPool can crash for threads > 1)
+        mt = reference_mt_probe(os.cpu_count() or 1)
+        detail["all_host_threads_probe"] = mt
+        if mt.get("completed") and mt["threads"] > 1:
+            v_mt = mt["knn_s"] + detail["t_init"] + mt["per_sweep_s"] * sweeps_total + (detail["t_extract_verify"] or 0.0)
+            detail["one_thread_projection_s"] = v
+            line["cpu_baseline"] = {
+                "value": v_mt, "unit": "s", "cores": mt["threads"], "kind": "reference", "cpu_model": _cpu_model(),
+                "sample": (f"unmodified reference (oracle/_ref) with {mt['threads']} threads: build_knn_graph + "
+                           f"{mt['sweeps_per_attempt']} Jacobi sweeps (child processes, median of the completed "
+                           f"attempts) + init and extract/verify on the converged lambda (1 thread); projected to "
+                           f"{sweeps_total} sweeps (the --impl reference arm times a complete stock full_solve)"),
+                "detail": detail}
+        else:
+            line["cpu_baseline"] = {
+                "value": v, "unit": "s", "cores": 1, "kind": "reference", "cpu_model": _cpu_model(),
+                "sample": (f"unmodified reference (oracle/_ref): build_knn_graph + init + {REF_SAMPLE_SWEEPS} Jacobi "
+                           f"sweeps + extract/verify on the converged lambda, 1 thread; projected to "
+                           f"{sweeps_total} sweeps (the --impl reference arm times a complete stock full_solve)"),
+                "detail": detail}
     # multi-rank legs: each agrees across ranks (all-reduce of an ok flag) before its collectives,
     # so a rank that fails its local setup makes every rank skip together instead of hanging
     if sharded_ctx is not None:
