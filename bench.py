@@ -251,7 +251,7 @@ def reference_mt_probe(threads: int, attempts: int = 3, sweeps: int = 200):
     done, crashed, knn, per = 0, 0, [], []
     for _ in range(attempts):
         try:
-            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=60)
         except subprocess.TimeoutExpired:
             crashed += 1
             continue
@@ -286,7 +286,7 @@ def reference_full_solve_threads(threads: int, attempts: int = 3):
     failed = 0
     for _ in range(attempts):
         try:
-            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900)
+            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
         except subprocess.TimeoutExpired:
             failed += 1
             continue
