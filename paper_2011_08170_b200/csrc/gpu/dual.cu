@@ -787,6 +787,9 @@ __device__ __forceinline__ void row_scan(double (&sv)[B + 1], double lv, const d
 #ifndef F2M_BANK_LAYOUT
 #define F2M_BANK_LAYOUT 1  // bank-aware initial slot order of the resident rows (layout_banks)
 #endif
+#ifndef F2M_LAYOUT_AUG
+#define F2M_LAYOUT_AUG 1  // one-step augmenting paths in the warp layout
+#endif
 #ifdef F2M_HEAD_STATS  // debug build: repaired rows, printed at exit
 __device__ unsigned long long g_head_stats[8];
 #define F2M_HEAD_COUNT(i) atomicAdd(&g_head_stats[i], 1ull)
@@ -1008,6 +1011,84 @@ __device__ __noinline__ void layout_banks(int B, double* cst_s, ushort4* lid4, i
   }
 }
 
+// layout_banks run by a whole warp (same greedy, same result): the lanes scan one row's remaining
+// candidate columns at once (lane i: column j + i) and a ballot picks the first acceptable one, so
+// a (row, column) step costs one shared-memory load per lane instead of a serial scan. Needs
+// w <= 32 (the caller falls back to layout_banks otherwise). wd: this warp's 16-word scratch.
+__device__ __forceinline__ void layout_banks_warp(int B, double* cst_s, ushort4* lid4, int4 sl, int l0, int nrows,
+                                               uint16_t* wd) {
+  uint16_t* lid = reinterpret_cast<uint16_t*>(lid4);
+  const int lane = threadIdx.x & 31;
+  const int w = sl.y, H = w > B + 1 ? B + 2 : 0;
+  auto ix = [&](int l, int k) { return (sl.z + 32 * (k >> 2) + l) * 4 + (k & 3); };
+  auto swap_cols = [&](int l, int j, int k) {  // lane 0 only
+    const int xj = ix(l, j), xk = ix(l, k);
+    const uint16_t t = lid[xj];
+    lid[xj] = lid[xk];
+    lid[xk] = t;
+    const double c = cst_s[sl.x + l + 32 * j];
+    cst_s[sl.x + l + 32 * j] = cst_s[sl.x + l + 32 * k];
+    cst_s[sl.x + l + 32 * k] = c;
+  };
+  for (int j = 0; j < w; ++j) {
+    const int hi = j < H ? H : w;
+    unsigned used = 0, shared = 0;
+    unsigned long long owner = 0;  // 4 bits per bank pair: the row (l - l0) using it
+    for (int l = l0; l < l0 + nrows; ++l) {
+      const int k = j + lane;
+      const bool in = k < hi;
+      const int q = in ? lid[ix(l, k)] : 0, b = q & 15;
+      const bool ok = in && (!((used >> b) & 1u) || wd[b] == q);
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      int pick = m ? j + __ffs(m) - 1 : -1;
+      if (pick < 0 && F2M_LAYOUT_AUG) {  // one-step augmenting path, candidates in column order
+        const unsigned cand = __ballot_sync(0xffffffffu, in);
+        for (unsigned cm = cand; cm && pick < 0; cm &= cm - 1) {
+          const int kk = j + __ffs(cm) - 1;
+          const int bb = __shfl_sync(0xffffffffu, b, kk - j);
+          if ((shared >> bb) & 1u) continue;
+          const int o = l0 + (int)((owner >> (4 * bb)) & 15);
+          const int k2 = j + 1 + lane;
+          const bool in2 = k2 < hi;
+          const int q2 = in2 ? lid[ix(o, k2)] : 0;
+          const unsigned m2 = __ballot_sync(0xffffffffu, in2 && !((used >> (q2 & 15)) & 1u));
+          if (m2) {
+            const int k2s = j + __ffs(m2);
+            const int q2s = __shfl_sync(0xffffffffu, q2, k2s - (j + 1));
+            if (lane == 0) {
+              swap_cols(o, j, k2s);
+              wd[q2s & 15] = (uint16_t)q2s;
+            }
+            __syncwarp();
+            used |= 1u << (q2s & 15);
+            owner = (owner & ~(15ull << (4 * (q2s & 15)))) | ((unsigned long long)(o - l0) << (4 * (q2s & 15)));
+            used &= ~(1u << bb);
+            pick = kk;
+          }
+        }
+      }
+#ifdef F2M_HEAD_STATS
+      if (lane == 0) {
+        F2M_HEAD_COUNT(j < H ? 4 : 5);
+        if (pick < 0) F2M_HEAD_COUNT(j < H ? 2 : 3);
+      }
+#endif
+      if (pick < 0) pick = j;
+      const int qp = __shfl_sync(0xffffffffu, q, pick - j);
+      if (lane == 0 && pick != j) swap_cols(l, j, pick);
+      const int bq = qp & 15;
+      if ((used >> bq) & 1u) {
+        shared |= 1u << bq;
+      } else {
+        used |= 1u << bq;
+        if (lane == 0) wd[bq] = (uint16_t)qp;
+        owner = (owner & ~(15ull << (4 * bq))) | ((unsigned long long)(l - l0) << (4 * bq));
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int B, bool RES, int NT, bool PAIR>
 __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* ctl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1016,6 +1097,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   __shared__ volatile int s_done;  // sweeps completed by the compute warps
   __shared__ volatile int s_exit;
   __shared__ unsigned long long s_word;
+  __shared__ uint16_t s_lw[NT / 32][16];  // layout_banks_warp scratch, one per warp
   // CTAs 0..G-1 own the partition; the last CTA of the launch (alone on its SM) is the master.
   // Multi-GPU: this launch's CTAs are the partition CTAs cta_base.. of g_total.
   const int G = a.npeers ? a.g_total : (int)gridDim.x - 1;
@@ -1102,9 +1184,12 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       __syncthreads();
       for (int lp = tid; lp < own; lp += blockDim.x) layout_head(B, cst_s, lid4, slc[lp >> 5], lp & 31, regA[lp], regA);
       __syncthreads();
-      for (int hs = tid; hs < 2 * ns; hs += blockDim.x) {  // one thread per half-slice
+      // one warp per half-slice (one thread when a slice is wider than 32 slots)
+      for (int hs = warp; hs < 2 * ns; hs += nwarps) {
         const int l0 = 16 * (hs & 1), nrows = min(16, own - 32 * (hs >> 1) - l0);
-        if (nrows > 0) layout_banks(B, cst_s, lid4, slc[hs >> 1], l0, nrows);
+        if (nrows <= 0) continue;
+        if (slc[hs >> 1].y <= 32) layout_banks_warp(B, cst_s, lid4, slc[hs >> 1], l0, nrows, s_lw[warp]);
+        else if (lane == 0) layout_banks(B, cst_s, lid4, slc[hs >> 1], l0, nrows);
       }
     }
   }
