@@ -371,10 +371,10 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   launched("grid_params");
   GridParams hp;
   static_assert(sizeof(GridParams) <= 8 * sizeof(int64_t), "pinned scratch slots 50-57");
+  // the grid's dimensions come back with the edge count's synchronisation below; until then the
+  // cell arrays are sized by k_grid_params' bound gx * gy <= 64 + 8n (the unused cells stay empty)
   F2M_CUDA(cudaMemcpyAsync(pinned_scratch() + 50, gp.get(), sizeof(hp), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
-  std::memcpy(&hp, pinned_scratch() + 50, sizeof(hp));
-  const int64_t cells = (int64_t)hp.gx * hp.gy;
+  const int64_t cells = 64 + 8 * (int64_t)n;
   DBuf<int32_t> cell_of(n, s), cnt(cells + 1, s), off(cells + 1, s), cur(cells, s), ids(n, s);
   DBuf<double2> pts(n, s);
   F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (cells + 1), s));
@@ -444,6 +444,7 @@ f2m_graph* knn_build_device(int n, const double* xy, bool xy_on_host, int rounde
   F2M_CUDA(cudaMemcpyAsync(pinned_scratch() + 58, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
   m = pinned_scratch()[58];
+  std::memcpy(&hp, pinned_scratch() + 50, sizeof(hp));  // copied before the synchronisation above
   t.m = m;
   t.eu.alloc(m, s);
   t.ev.alloc(m, s);
