@@ -352,9 +352,10 @@ __global__ void k_halo_keys(int n, int64_t nslices, const int64_t* __restrict__ 
 }
 
 __global__ void k_halo_split(int64_t h, const uint64_t* __restrict__ keys, int qbits, int32_t* __restrict__ halo,
-                             int32_t* __restrict__ cnt) {
+                             int32_t* __restrict__ cnt, const int64_t* __restrict__ dh = nullptr) {
+  // dh: the entry count on the device (the grid covers an upper bound h, no host round trip)
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= h) return;
+  if (i >= h || (dh && i >= *dh)) return;
   halo[i] = (int32_t)(keys[i] & ((1ull << qbits) - 1));
   // keys are sorted by CTA: lanes with the same CTA add once (a handful of contended counters)
   const int c = (int)(keys[i] >> qbits);
@@ -505,7 +506,8 @@ static void build_local_index(Topology& t) {
   const int key_bits = bit_width(G) + qbits;  // 2^bit_width(G) > G - 1: the all-ones sentinel is unused
   const uint64_t sentinel = (key_bits >= 64) ? ~0ULL : ((1ull << key_bits) - 1);
   DBuf<uint64_t> k0(std::max<int64_t>(slots, 1), s), k1(std::max<int64_t>(slots, 1), s);
-  DBuf<int64_t> nsel(1, s);
+  DBuf<int64_t> nsel(1, s), hcnt(1, s);
+  F2M_CUDA(cudaMemsetAsync(hcnt.get(), 0, sizeof(int64_t), s));
   int64_t h = 0;
   if (slots > 0) {
     k_halo_keys<<<grid_for(t.nslices * 32, 256), 256, 0, s>>>(n, t.nslices, t.sptr.get(), t.scol.get(),
@@ -522,21 +524,18 @@ static void build_local_index(Topology& t) {
     DBuf<char> tb2(tmp, s);
     F2M_CUDA(cub::DeviceSelect::Unique(tb2.get(), tmp, k1.get(), k0.get(), nsel.get(), slots, s));
     launched("unique_halo");
-    DBuf<int64_t> hcnt(1, s);
     k_drop_sentinel<<<1, 1, 0, s>>>(nsel.get(), k0.get(), sentinel, hcnt.get());
     launched("drop_sentinel");
-    int64_t* hs = pinned_scratch();
-    F2M_CUDA(cudaMemcpyAsync(hs, hcnt.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaStreamSynchronize(s));
-    h = hs[0];
   }
-  t.halo.alloc(std::max<int64_t>(h, 1), s);
+  // the halo count comes back with the sizes below: until then the halo list is sized (and the
+  // split launched) for its bound, the slot count
+  t.halo.alloc(std::max<int64_t>(slots, 1), s);
   t.halo_off.alloc(G + 1, s);
   {
     DBuf<int32_t> cnt(G + 1, s);
     F2M_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (G + 1), s));
-    if (h > 0) {
-      k_halo_split<<<grid_for(h, 256), 256, 0, s>>>(h, k0.get(), qbits, t.halo.get(), cnt.get());
+    if (slots > 0) {
+      k_halo_split<<<grid_for(slots, 256), 256, 0, s>>>(slots, k0.get(), qbits, t.halo.get(), cnt.get(), hcnt.get());
       launched("halo_split");
     }
     size_t tmp = 0;
@@ -557,7 +556,9 @@ static void build_local_index(Topology& t) {
     int64_t* hs = pinned_scratch();  // both sizes with one synchronisation
     F2M_CUDA(cudaMemcpyAsync(hs + 1, ml.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaMemcpyAsync(hs + 2, ms.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 3, hcnt.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
+    h = hs[3];
     t.max_local = reinterpret_cast<const int*>(hs + 1)[0];
     t.max_halo = reinterpret_cast<const int*>(hs + 1)[1];
     t.max_cta_slots = hs[2];
