@@ -364,15 +364,19 @@ __global__ void k_halo_split(int64_t h, const uint64_t* __restrict__ keys, int q
 }
 
 __global__ void k_local_sizes(int ctas, int n, const int32_t* __restrict__ lo, const int32_t* __restrict__ hoff,
-                              const int64_t* __restrict__ sptr, int* __restrict__ max_local,
-                              unsigned long long* __restrict__ max_slots) {
+                              const int64_t* __restrict__ sptr, const int32_t* __restrict__ swidth,
+                              int* __restrict__ max_local, unsigned long long* __restrict__ max_slots) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ctas) return;
   int p0, p1;
   own_range(c, n, lo, p0, p1);
   atomicMax(max_local, (p1 - p0) + (hoff[c + 1] - hoff[c]));
   atomicMax(max_local + 1, hoff[c + 1] - hoff[c]);  // halo entries alone
+  atomicMax(max_local + 2, lo[c + 1] - lo[c]);      // slices
   atomicMax(max_slots, (unsigned long long)(sptr[lo[c + 1]] - sptr[lo[c]]));
+  unsigned long long l4 = 0;  // packed local-index entries (ushort4, widths padded to 4)
+  for (int i = lo[c]; i < lo[c + 1]; ++i) l4 += 32ull * (unsigned)((swidth[i] + 3) / 4);
+  atomicMax(max_slots + 1, l4);
 }
 
 __global__ void k_slot_lidx(int n, int64_t nslices, const int64_t* __restrict__ sptr,
@@ -544,24 +548,43 @@ static void build_local_index(Topology& t) {
     F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.halo_off.get(), G + 1, s));
     launched("scan_halo");
   }
-  // sizes
+  // LL publication offsets (boundary nodes of each CTA, in position order)
+  t.boff.alloc(G + 1, s);
   {
-    DBuf<int> ml(2, s);
-    DBuf<unsigned long long> ms(1, s);
-    F2M_CUDA(cudaMemsetAsync(ml.get(), 0, 2 * sizeof(int), s));
-    F2M_CUDA(cudaMemsetAsync(ms.get(), 0, sizeof(unsigned long long), s));
-    k_local_sizes<<<grid_for(G, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.halo_off.get(), t.sptr.get(), ml.get(),
-                                                   ms.get());
+    DBuf<int32_t> cnt(G + 1, s);
+    k_boundary_counts<<<grid_for(G + 1, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.cta_nint.get(), cnt.get());
+    launched("boundary_counts");
+    size_t tmp = 0;
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.boff.get(), G + 1, s));
+    DBuf<char> tb(tmp, s);
+    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.boff.get(), G + 1, s));
+    launched("scan_boundary");
+  }
+  // sizes: local index space, halo, slots, slices, packed indices, halo count and boundary count
+  // with ONE synchronisation
+  int max_slices = 0;
+  int64_t max_lid4 = 0;  // resident: packed local indices, 4 slots per 8-byte entry, widths padded to 4
+  {
+    DBuf<int> ml(3, s);
+    DBuf<unsigned long long> ms(2, s);
+    F2M_CUDA(cudaMemsetAsync(ml.get(), 0, 3 * sizeof(int), s));
+    F2M_CUDA(cudaMemsetAsync(ms.get(), 0, 2 * sizeof(unsigned long long), s));
+    k_local_sizes<<<grid_for(G, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.halo_off.get(), t.sptr.get(),
+                                                   t.swidth.get(), ml.get(), ms.get());
     launched("local_sizes");
-    int64_t* hs = pinned_scratch();  // both sizes with one synchronisation
-    F2M_CUDA(cudaMemcpyAsync(hs + 1, ml.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaMemcpyAsync(hs + 2, ms.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaMemcpyAsync(hs + 3, hcnt.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    int64_t* hs = pinned_scratch();
+    F2M_CUDA(cudaMemcpyAsync(hs + 1, ml.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 4, ms.get(), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 6, hcnt.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    F2M_CUDA(cudaMemcpyAsync(hs + 7, t.boff.get() + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     F2M_CUDA(cudaStreamSynchronize(s));
-    h = hs[3];
+    h = hs[6];
     t.max_local = reinterpret_cast<const int*>(hs + 1)[0];
     t.max_halo = reinterpret_cast<const int*>(hs + 1)[1];
-    t.max_cta_slots = hs[2];
+    max_slices = reinterpret_cast<const int*>(hs + 1)[2];
+    t.max_cta_slots = hs[4];
+    max_lid4 = hs[5];
+    t.nboundary = reinterpret_cast<const int32_t*>(hs + 7)[0];
   }
   const size_t limit = sweep_smem_limit(t.dev);
   const size_t lam_bytes = (size_t)t.max_local * sizeof(double);
@@ -582,18 +605,9 @@ static void build_local_index(Topology& t) {
                                                              t.sdest.get(), t.row_nhalo.get());
     launched("halo_last");
   }
-  // LL publication indices (boundary nodes of each CTA, in position order)
-  t.boff.alloc(G + 1, s);
+  // LL publication indices of the halo entries
   t.halo_pub.alloc(std::max<int64_t>(h, 1), s);
   {
-    DBuf<int32_t> cnt(G + 1, s);
-    k_boundary_counts<<<grid_for(G + 1, 128), 128, 0, s>>>(G, n, t.cta_lo.get(), t.cta_nint.get(), cnt.get());
-    launched("boundary_counts");
-    size_t tmp = 0;
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), t.boff.get(), G + 1, s));
-    DBuf<char> tb(tmp, s);
-    F2M_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, cnt.get(), t.boff.get(), G + 1, s));
-    launched("scan_boundary");
     if (h > 0) {
       k_halo_pub<<<grid_for(h, 256), 256, 0, s>>>(h, t.halo.get(), cos.get(), t.cta_lo.get(), t.cta_nint.get(),
                                                   t.boff.get(), t.halo_pub.get());
@@ -603,25 +617,6 @@ static void build_local_index(Topology& t) {
   // [lam regions][halo LL ids (max halo ints, 16-byte aligned)][resident: cost + local index per slot]
   const size_t lam_aligned = (lam_bytes + 15) & ~size_t(15);
   const size_t ids_bytes = (((size_t)t.max_halo * sizeof(int)) + 15) & ~size_t(15);
-  // boundary count and the per-CTA slice table size (v5: (slot offset, width) per slice, 16-byte
-  // aligned) from one stream synchronisation
-  int max_slices = 0;
-  int64_t max_lid4 = 0;  // resident: packed local indices, 4 slots per 8-byte entry, widths padded to 4
-  {
-    int32_t* hs = reinterpret_cast<int32_t*>(pinned_scratch());
-    F2M_CUDA(cudaMemcpyAsync(hs, t.boff.get() + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> lo(G + 1), wid(t.nslices);
-    F2M_CUDA(cudaMemcpyAsync(lo.data(), t.cta_lo.get(), sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaMemcpyAsync(wid.data(), t.swidth.get(), sizeof(int32_t) * t.nslices, cudaMemcpyDeviceToHost, s));
-    F2M_CUDA(cudaStreamSynchronize(s));
-    t.nboundary = hs[0];
-    for (int c = 0; c < G; ++c) {
-      max_slices = std::max(max_slices, lo[c + 1] - lo[c]);
-      int64_t l4 = 0;
-      for (int i = lo[c]; i < lo[c + 1]; ++i) l4 += 32 * ((wid[i] + 3) / 4);
-      max_lid4 = std::max(max_lid4, l4);
-    }
-  }
   t.max_cta_lid4 = max_lid4;
   const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int4);
   const size_t resident_bytes = 2 * lam_aligned + ids_bytes + (size_t)t.max_cta_slots * sizeof(double) +
@@ -637,7 +632,6 @@ static void build_local_index(Topology& t) {
   t.v2 = true;
   t.resident = resident_bytes <= limit;
   t.smem_bytes = t.resident ? resident_bytes : streaming_bytes;
-  F2M_CUDA(cudaStreamSynchronize(s));
 }
 
 void finalize_topology(Topology& t) {
