@@ -361,10 +361,10 @@ static int64_t select_flagged(const T* in, const uint8_t* flags, T* out, int64_t
   DBuf<char> tb(tmp, s);
   F2M_CUDA(cub::DeviceSelect::Flagged(tb.get(), tmp, in, flags, out, nsel.get(), count, s));
   launched("select_flagged");
-  int64_t h = 0;
-  F2M_CUDA(cudaMemcpyAsync(&h, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  int64_t* ps = pinned_scratch();  // page-locked: a pageable destination would stage the copy
+  F2M_CUDA(cudaMemcpyAsync(ps + 12, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
-  return h;
+  return ps[12];
 }
 
 void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, double* d_x) {
@@ -390,24 +390,30 @@ void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, dou
     k_check_nodes<<<grid_for(n, 256), 256, 0, s>>>(n, negd.get(), zerod.get(), residual.get(), first.get());
     launched("check_nodes");
   }
-  unsigned long long hfirst = 0;
-  F2M_CUDA(cudaMemcpyAsync(&hfirst, first.get(), sizeof(hfirst), cudaMemcpyDeviceToHost, s));
-  F2M_CUDA(cudaStreamSynchronize(s));
-  if (hfirst != ~0ULL) {
-    const int v = (int)(hfirst / 2);
+  // the node check's verdict comes back with the next synchronisation (the zero-band selection)
+  unsigned long long* hfirst = reinterpret_cast<unsigned long long*>(pinned_scratch() + 13);
+  F2M_CUDA(cudaMemcpyAsync(hfirst, first.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  auto check_nodes = [&] {  // primal.cpp:155-175 order: node degrees before the zero components
+    if (*hfirst == ~0ULL) return;
+    const int v = (int)(*hfirst / 2);
     int nd = 0;
     F2M_CUDA(cudaMemcpy(&nd, negd.get() + v, sizeof(int), cudaMemcpyDeviceToHost));
-    if (hfirst % 2 == 0)
+    if (*hfirst % 2 == 0)
       throw Error(F2M_E_DEGENERATE, "node " + std::to_string(v) + " has " + std::to_string(nd) + " tight edges (> 2)");
     throw Error(F2M_E_DEGENERATE, "node " + std::to_string(v) + " needs " + std::to_string(2 - nd) +
                                       " more units but has no zero-band edge");
+  };
+  if (m == 0) {
+    F2M_CUDA(cudaStreamSynchronize(s));
+    check_nodes();
+    return;
   }
-  if (m == 0) return;
   // zero-band edges, ascending
   DBuf<int32_t> eids(m, s), zedges(m, s);
   k_iota_n<<<grid_for(m, 256), 256, 0, s>>>((int)m, eids.get());
   launched("iota");
   const int64_t z = select_flagged<int32_t>(eids.get(), zflag.get(), zedges.get(), m, s);
+  check_nodes();
   if (z == 0) return;
   DBuf<int> parent(n, s);
   k_iota_n<<<grid_for(n, 256), 256, 0, s>>>(n, parent.get());
@@ -437,9 +443,10 @@ void extract_device(const f2m_graph& g, const double* d_lam_pos, double tol, dou
   k_components<<<grid_for(ncomp * 32, 128), 128, 0, s>>>(ncomp, z, heads.get(), k1.get(), t.eu.get(), t.ev.get(),
                                                         g.cost.get(), residual.get(), d_x, ebits, fail.get());
   launched("zero_components");
-  unsigned long long hf = 0;
-  F2M_CUDA(cudaMemcpyAsync(&hf, fail.get(), sizeof(hf), cudaMemcpyDeviceToHost, s));
+  unsigned long long* hfp = reinterpret_cast<unsigned long long*>(pinned_scratch() + 14);
+  F2M_CUDA(cudaMemcpyAsync(hfp, fail.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   F2M_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long hf = *hfp;
   if (hf != ~0ULL) {
     const unsigned low = (unsigned)(hf & 0xffffffffu);
     const unsigned mc = low & 0x7fffffffu;
