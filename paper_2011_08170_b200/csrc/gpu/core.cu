@@ -1027,33 +1027,44 @@ extern "C" int f2m_graph_incidence(const f2m_graph* g, int64_t* offsets, int32_t
   });
 }
 
+namespace f2mgpu {
+// validate_graph (graph.cpp:242-277) on the device: the first defect's {edge << 2 | kind} goes to
+// the page-locked *h_first (all ones: none) without a synchronisation
+void validate_graph_async(const f2m_graph& g, unsigned long long* h_first) {
+  const Topology& t = *g.topo;
+  cudaStream_t s = t.stream;
+  *h_first = ~0ULL;
+  if (t.m <= 0) return;
+  DBuf<unsigned long long> first(1, s);
+  F2M_CUDA(cudaMemsetAsync(first.get(), 0xff, sizeof(unsigned long long), s));
+  k_validate<<<grid_for(t.m, 256), 256, 0, s>>>(t.m, t.eu.get(), t.ev.get(), g.cost.get(), first.get());
+  launched("validate");
+  F2M_CUDA(cudaMemcpyAsync(h_first, first.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+}
+// after a synchronisation of the graph's stream: throw the defect validate_graph_async found
+void validate_graph_check(const f2m_graph& g, unsigned long long h) {
+  if (h == ~0ULL) return;
+  const Topology& t = *g.topo;
+  const int64_t e = (int64_t)(h >> 2);
+  const int kind = (int)(h & 3);
+  int32_t u = 0, v = 0;
+  F2M_CUDA(cudaMemcpy(&u, t.eu.get() + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  F2M_CUDA(cudaMemcpy(&v, t.ev.get() + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (kind == 1) throw Error(F2M_E_STRUCTURE, "self-loop at node " + std::to_string(u));
+  if (kind == 2) throw Error(F2M_E_STRUCTURE, "duplicate edge (" + std::to_string(u) + ", " + std::to_string(v) + ")");
+  throw Error(F2M_E_STRUCTURE, "negative cost on edge (" + std::to_string(u) + ", " + std::to_string(v) + ")");
+}
+}  // namespace f2mgpu
+
 extern "C" int f2m_graph_validate(const f2m_graph* g, int* min_degree, int* max_degree,
                                   int64_t* edges) {
   return guard([&] {
     const Topology& t = *g->topo;
     F2M_CUDA(cudaSetDevice(t.dev));
-    cudaStream_t s = t.stream;
-    if (t.m > 0) {
-      DBuf<unsigned long long> first(1, s);
-      F2M_CUDA(cudaMemsetAsync(first.get(), 0xff, sizeof(unsigned long long), s));
-      k_validate<<<grid_for(t.m, 256), 256, 0, s>>>(t.m, t.eu.get(), t.ev.get(), g->cost.get(), first.get());
-      launched("validate");
-      unsigned long long h = 0;
-      F2M_CUDA(cudaMemcpyAsync(&h, first.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
-      F2M_CUDA(cudaStreamSynchronize(s));
-      if (h != ~0ULL) {
-        const int64_t e = (int64_t)(h >> 2);
-        const int kind = (int)(h & 3);
-        int32_t u = 0, v = 0;
-        F2M_CUDA(cudaMemcpy(&u, t.eu.get() + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        F2M_CUDA(cudaMemcpy(&v, t.ev.get() + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        if (kind == 1) throw Error(F2M_E_STRUCTURE, "self-loop at node " + std::to_string(u));
-        if (kind == 2)
-          throw Error(F2M_E_STRUCTURE, "duplicate edge (" + std::to_string(u) + ", " + std::to_string(v) + ")");
-        throw Error(F2M_E_STRUCTURE,
-                    "negative cost on edge (" + std::to_string(u) + ", " + std::to_string(v) + ")");
-      }
-    }
+    unsigned long long* hf = reinterpret_cast<unsigned long long*>(pinned_scratch() + 15);
+    validate_graph_async(*g, hf);
+    F2M_CUDA(cudaStreamSynchronize(t.stream));
+    validate_graph_check(*g, *hf);
     const int mn = t.n > 0 ? t.min_deg : 0;
     if (min_degree) *min_degree = mn;
     if (max_degree) *max_degree = t.max_deg;

@@ -167,6 +167,12 @@ struct Topology {
 struct MultiPlan;  // multi.cu: per-graph replicas + rings of the single-process multi-GPU solve
 
 }  // namespace f2mgpu
+struct f2m_graph;
+namespace f2mgpu {
+void validate_graph_async(const f2m_graph& g, unsigned long long* h_first);
+void validate_graph_check(const f2m_graph& g, unsigned long long h);
+
+}  // namespace f2mgpu
 
 struct f2m_graph {
   std::shared_ptr<f2mgpu::Topology> topo;

@@ -41,12 +41,11 @@ static double seconds_since(std::chrono::steady_clock::time_point t0) {
 static void full_solve_graph_device(const f2m_graph& g, const f2m_run_config& rc, DBuf<double>& d_x,
                                     DBuf<double>& d_lam, f2m_solve_outcome& out) {
   validate_run(rc);
-  {
-    int mn, mx;
-    int64_t m;
-    const int st = f2m_graph_validate(&g, &mn, &mx, &m);
-    if (st != F2M_OK) throw Error(st, f2m_last_error());
-  }
+  // validate_graph (solve.cpp:55) without a synchronisation of its own: its verdict is read after
+  // the first attempt's dual solve, before any result is used
+  unsigned long long* h_valid = reinterpret_cast<unsigned long long*>(pinned_scratch() + 15);
+  validate_graph_async(g, h_valid);
+  bool validated = false;
   const Topology& t = *g.topo;
   std::string last_failure = "no attempt made";
   double t_duals = 0.0, t_extract = 0.0;
@@ -66,7 +65,19 @@ static void full_solve_graph_device(const f2m_graph& g, const f2m_run_config& rc
     // it is read back (page-locked, asynchronously) with the extraction's synchronisations
     const bool same = jit == nullptr && rc.engine.b == 2;
     double* dual_async = reinterpret_cast<double*>(pinned_scratch() + 24);
-    solve_duals_device(attempt, rc.engine, nullptr, lam, conv, dual_async);
+    try {
+      solve_duals_device(attempt, rc.engine, nullptr, lam, conv, dual_async);
+    } catch (...) {
+      if (!validated) {  // a structural defect is the reference's first error
+        F2M_CUDA(cudaStreamSynchronize(t.stream));
+        validate_graph_check(g, *h_valid);
+      }
+      throw;
+    }
+    if (!validated) {  // solve_duals_device synchronised the stream
+      validate_graph_check(g, *h_valid);
+      validated = true;
+    }
     t_duals += seconds_since(ts);
 
     ts = std::chrono::steady_clock::now();
