@@ -1862,9 +1862,72 @@ __global__ void __launch_bounds__(256) k_init_local_midpoint(
   }
 }
 
+// make_initial_state (dual.cpp:194-208) with one thread per node: warps claim 32 consecutive
+// node ids at a time (ids start in order), each lane scans its node's row and waits (LL poll) only
+// for the neighbours with lower ids, exactly the values the reference's in-order pass has already
+// written. The kept multiset of the b+1 smallest is the warp form's, so lambda_0 is bit-identical;
+// the dependency chain (DAG depth ~26 at 100k) no longer queues behind one warp per node.
+template <int B>
+__global__ void __launch_bounds__(256) k_init_thread(
+    int n, const int32_t* __restrict__ perm, const int32_t* __restrict__ iperm,
+    const int32_t* __restrict__ deg, const int64_t* __restrict__ sptr,
+    const int32_t* __restrict__ scol, const double* __restrict__ scost, double* lam,
+    unsigned long long* ll, int* counter, int* err) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(counter, 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    const int v = base + lane;
+    if (v >= n) continue;
+    const int p = perm[v];
+    const int d = deg[p];
+    const int64_t rb = sptr[p >> 5] + (p & 31);
+    double sv[B + 1];
+#pragma unroll
+    for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
+    for (int j = 0; j < d; ++j) {
+      const int q = scol[rb + (int64_t)j * 32];
+      const double c = scost[rb + (int64_t)j * 32];
+      double other = 0.0;  // lambda of a higher-numbered (or the same) node is still 0
+      if (iperm[q] < v) {
+        const uint64_t t0 = globaltimer_ns();
+        unsigned long long w0, w1;
+        for (;;) {
+          ld_ll_raw(ll + 2 * (int64_t)q, w0, w1);
+          if (ll_ok(w0, w1, 1u)) break;
+          if (globaltimer_ns() - t0 > 20ull * 1000000000ull) {
+            atomicExch(err, 1);
+            break;
+          }
+        }
+        other = ll_val(w0, w1);
+      }
+      topk_insert<B>(sv, dsub(dsub(c, 0.0), other));  // ge.cost - lv - other, lv = 0 (dual.cpp:43)
+    }
+    const double val = d > B ? dmul(0.5, dadd(sv[B - 1], sv[B])) : 0.0;
+    st_ll(ll + 2 * (int64_t)p, val, 1u);
+    lam[p] = val;
+  }
+}
+
+#ifndef F2M_INIT_THREAD
+#define F2M_INIT_THREAD 1
+#endif
+
 template <int B>
 static void launch_init(const f2m_graph& g, double* d_lam, unsigned long long* ll, int* counter, int* err) {
   const Topology& t = *g.topo;
+  if (F2M_INIT_THREAD) {
+    // persistent: every thread of the grid is resident, so a claimed id's lower neighbours are held
+    // by running threads (ids are claimed in increasing order)
+    const int blocks = std::max(1, std::min<int>(grid_for(t.n, 256), device_props(t.dev).multiProcessorCount * 8));
+    k_init_thread<B><<<blocks, 256, 0, t.stream>>>(t.n, t.perm.get(), t.iperm.get(), t.deg.get(), t.sptr.get(),
+                                                  t.scol.get(), g.scost.get(), d_lam, ll, counter, err);
+    launched("init_thread");
+    return;
+  }
   // 4 CTAs (32 warps) per SM: measured 0.14 ms at 100k vs 0.23 ms with 8 (fewer warps spinning
   // on the id-order frontier, less contention on the claim counter)
   const int blocks = std::max(1, std::min<int>(grid_for((int64_t)t.n * 32, 256),
