@@ -1887,24 +1887,43 @@ __global__ void __launch_bounds__(256) k_init_thread(
     double sv[B + 1];
 #pragma unroll
     for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
-    for (int j = 0; j < d; ++j) {
-      const int q = scol[rb + (int64_t)j * 32];
-      const double c = scost[rb + (int64_t)j * 32];
-      double other = 0.0;  // lambda of a higher-numbered (or the same) node is still 0
-      if (iperm[q] < v) {
-        const uint64_t t0 = globaltimer_ns();
-        unsigned long long w0, w1;
-        for (;;) {
-          ld_ll_raw(ll + 2 * (int64_t)q, w0, w1);
-          if (ll_ok(w0, w1, 1u)) break;
-          if (globaltimer_ns() - t0 > 20ull * 1000000000ull) {
-            atomicExch(err, 1);
-            break;
-          }
+    // slots in chunks of 4: the LL words of all lower-id neighbours of a chunk are polled together
+    // (one L2 round trip per round, not one per neighbour)
+    for (int j0 = 0; j0 < d; j0 += 4) {
+      int q[4];
+      double c[4], other[4];
+      unsigned pend = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        other[u] = 0.0;  // lambda of a higher-numbered (or the same) node is still 0
+        c[u] = CUDART_INF;
+        q[u] = 0;
+        if (j0 + u < d) {
+          q[u] = scol[rb + (int64_t)(j0 + u) * 32];
+          c[u] = scost[rb + (int64_t)(j0 + u) * 32];
+          if (iperm[q[u]] < v) pend |= 1u << u;
         }
-        other = ll_val(w0, w1);
       }
-      topk_insert<B>(sv, dsub(dsub(c, 0.0), other));  // ge.cost - lv - other, lv = 0 (dual.cpp:43)
+      const uint64_t t0 = pend ? globaltimer_ns() : 0;
+      while (pend) {
+        unsigned long long w0[4], w1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pend & (1u << u)) ld_ll_raw(ll + 2 * (int64_t)q[u], w0[u], w1[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if ((pend & (1u << u)) && ll_ok(w0[u], w1[u], 1u)) {
+            other[u] = ll_val(w0[u], w1[u]);
+            pend &= ~(1u << u);
+          }
+        if (pend && globaltimer_ns() - t0 > 20ull * 1000000000ull) {
+          atomicExch(err, 1);
+          break;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < d) topk_insert<B>(sv, dsub(dsub(c[u], 0.0), other[u]));  // ge.cost - lv - other, lv = 0
     }
     const double val = d > B ? dmul(0.5, dadd(sv[B - 1], sv[B])) : 0.0;
     st_ll(ll + 2 * (int64_t)p, val, 1u);
