@@ -632,6 +632,12 @@ static void build_local_index(Topology& t) {
   t.v2 = true;
   t.resident = resident_bytes <= limit;
   t.smem_bytes = t.resident ? resident_bytes : streaming_bytes;
+  // eight multiplier regions (the last 8 sweeps) when they fit: no per-sweep global copy of lambda
+  t.lam_ring = 2;
+  if (t.resident && F2M_LAM_RING8 && resident_bytes + 6 * lam_aligned <= limit) {
+    t.lam_ring = 8;
+    t.smem_bytes = resident_bytes + 6 * lam_aligned;
+  }
 }
 
 void finalize_topology(Topology& t) {

@@ -506,6 +506,8 @@ struct Sweep4Args {
   unsigned long long* const* ll_peers;
   unsigned long long* const* cmax_peers;
   const uint32_t* __restrict__ ll_mask;  // [nb] ranks that read each boundary node
+  int lam_ring;  // resident: multiplier regions in shared memory (2, or 8: the last 8 sweeps stay in
+                 // shared memory and only the stopping sweep's result is written to gl at exit)
 };
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
@@ -1139,7 +1141,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   const int nslots = (int)(a.sptr[s_hi] - slot0);
   double* regA = reinterpret_cast<double*>(smem);
   double* regB = regA + (RES ? a.lam_stride : 0);
-  int* halo_s = reinterpret_cast<int*>(regA + (RES ? 2 : 1) * a.lam_stride);
+  // resident: lam_ring regions; sweep s reads region s % ring and writes region (s + 1) % ring
+  const int ring = RES ? a.lam_ring : 1;
+  auto region = [&](int i) { return regA + (size_t)(RES ? (ring == 8 ? (i & 7) : (i & 1)) : 0) * a.lam_stride; };
+  const bool gl_each_sweep = !RES || ring != 8;  // else the result goes to gl once, at exit
+  int* halo_s = reinterpret_cast<int*>(regA + (RES ? ring : 1) * a.lam_stride);
   double* cst_s = reinterpret_cast<double*>(halo_s + a.halo_stride);
   // resident local indices, packed 4 slots per lane: slice t's slot (j, lane) is component j % 4 of
   // lid4[slc[t].z + 32 (j / 4) + lane] — one 8-byte load per lane per 4 slots instead of four 2-byte
@@ -1211,7 +1217,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       const int need = (RES && a.runahead) ? s - 1 : s;  // the region being filled is no longer read
       while (s_done < need && !s_exit) __nanosleep(32);
       if (s_exit) break;
-      double* lam = (RES && (s & 1)) ? regB : regA;
+      double* lam = region(s);
       const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
       const unsigned long long* llin = a.ll + (size_t)(s % kLLRing) * a.nb * 2;
       const uint64_t t0 = globaltimer_ns();
@@ -1282,11 +1288,12 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #ifdef F2M_WARP_PROFILE
   unsigned long long prof[kProfFields] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
+  int s_stop_final = -1;
   for (int s = 0;; ++s) {
     F2M_PROF_T(t0);
     if (tid == 0) F2M_TRACE_EV(s, 0);
-    double* lam = (RES && (s & 1)) ? regB : regA;
-    double* lam_next = (s & 1) ? regA : regB;
+    double* lam = region(s);
+    double* lam_next = RES ? region(s + 1) : ((s & 1) ? regA : regB);
     const double* gin = (a.gl + (size_t)(s & 7) * a.gstride);
     double* gout = (a.gl + (size_t)((s + 1) & 7) * a.gstride);
     if (!RES) {
@@ -1345,7 +1352,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
           if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
-          gout[p] = nl;
+          if (gl_each_sweep) gout[p] = nl;
           lam_next[lp] = nl;
           const double ad = fabs(d);
           mx = mx < ad ? ad : mx;
@@ -1384,7 +1391,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           const double d = delta_of<B>(sv, a.update);
           const double nl = dadd(lv, dmul(a.eta, d));
           if (lp >= nint) publish_ll(a, llout, bo + lp, nl, (unsigned)s + 1);
-          gout[p] = nl;
+          if (gl_each_sweep) gout[p] = nl;
           if (RES) lam_next[lp] = nl;
           const double ad = fabs(d);
           mx = mx < ad ? ad : mx;
@@ -1433,7 +1440,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       }
       const double d = delta_of<B>(sv, a.update);
       const double nl = dadd(lv, dmul(a.eta, d));
-      gout[p] = nl;
+      if (gl_each_sweep) gout[p] = nl;
       if (RES) lam_next[lp] = nl;
       const double ad = fabs(d);
       mx = mx < ad ? ad : mx;
@@ -1485,7 +1492,10 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
         s_done = s + 1;
       }
     }
-    if (s_stop[s & 1] >= 0) break;
+    if (s_stop[s & 1] >= 0) {
+      s_stop_final = s_stop[s & 1];
+      break;
+    }
   }
 #ifdef F2M_WARP_PROFILE
   if (lane == 0 && c < kProfCtas && warp < kProfWarps) {
@@ -1499,6 +1509,13 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
     for (int f = 0; f < kProfFields; ++f) g_wprof[c][warp][f] = prof[f];
   }
 #endif
+  if (!gl_each_sweep && s_stop_final >= 0) {
+    // the stopping sweep k's result (shared-memory region (k + 1) % 8, never overwritten: a CTA runs
+    // at most sweep k + 7, see the verdict lag) goes to gl buffer (k + 1) % 8, where the host reads it
+    const double* res = region(s_stop_final + 1);
+    double* gdst_out = a.gl + (size_t)((s_stop_final + 1) & 7) * a.gstride + p0;
+    for (int i = tid; i < own; i += cthreads) gdst_out[i] = res[i];
+  }
   if (tid == 0) s_exit = 1;
 #ifdef F2M_HEAD_STATS
   if (tid == 0 && c == 0)
@@ -1752,6 +1769,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.max_sweeps = max_sweeps;
     a.record = d_record;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.lam_ring = t.resident ? t.lam_ring : 2;
     a.halo_stride = (t.max_halo + 3) & ~3;
     a.lid4_stride = (int)t.max_cta_lid4;
     a.cta_base = 0;
@@ -2553,6 +2571,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.max_sweeps = max_sweeps;
     a.record = nullptr;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
+    a.lam_ring = t.resident ? t.lam_ring : 2;
     a.halo_stride = (t.max_halo + 3) & ~3;
     a.lid4_stride = (int)t.max_cta_lid4;
     a.cta_base = rank * Gp;

@@ -113,6 +113,10 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+#ifndef F2M_LAM_RING8
+#define F2M_LAM_RING8 1
+#endif
+
 // ---------------------------------------------------------------- graph structures
 struct Topology {
   int dev = 0;
@@ -160,6 +164,7 @@ struct Topology {
   int64_t max_cta_slots = 0;   // max over CTAs of padded slots
   int64_t max_cta_lid4 = 0;    // max over CTAs of packed local-index entries (ushort4, widths padded to 4)
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
+  int lam_ring = 2;            // resident: shared-memory multiplier regions (8 when they fit, see dual.cu)
   int partition_override = 0;  // > 0: partition CTA count for finalize_topology (multi-GPU replicas)
   ~Topology();
 };
