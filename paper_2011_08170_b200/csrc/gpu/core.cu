@@ -619,8 +619,8 @@ static void build_local_index(Topology& t) {
   const size_t ids_bytes = (((size_t)t.max_halo * sizeof(int)) + 15) & ~size_t(15);
   t.max_cta_lid4 = max_lid4;
   const size_t slice_bytes = 16 + (size_t)max_slices * sizeof(int4);
-  const size_t resident_bytes = 2 * lam_aligned + ids_bytes + (size_t)t.max_cta_slots * sizeof(double) +
-                                (size_t)max_lid4 * 8 + slice_bytes;
+  size_t resident_bytes = 2 * lam_aligned + ids_bytes + (size_t)t.max_cta_slots * sizeof(double) +
+                          (size_t)max_lid4 * 8 + slice_bytes;
   const size_t streaming_bytes = lam_aligned + ids_bytes + slice_bytes;
   if (streaming_bytes > limit) return;  // v1 kernel
   // The sweep kernel keeps per-sweep CTA maxima in a ring of kCmaxRing (64) slots. A CTA starts
@@ -631,6 +631,12 @@ static void build_local_index(Topology& t) {
   if (G > 4096) return;  // v1 kernel
   t.v2 = true;
   t.resident = resident_bytes <= limit;
+  // per-row tail budgets (8 bytes per own row, after the slice table) when they fit
+  t.row_skip = 0;
+  if (t.resident && F2M_ROW_SKIP && resident_bytes + 16 + (size_t)t.max_local * 8 <= limit) {
+    t.row_skip = 1;
+    resident_bytes += 16 + (size_t)t.max_local * 8;
+  }
   t.smem_bytes = t.resident ? resident_bytes : streaming_bytes;
   // eight multiplier regions (the last 8 sweeps) when they fit: no per-sweep global copy of lambda
   t.lam_ring = 2;

@@ -508,6 +508,7 @@ struct Sweep4Args {
   const uint32_t* __restrict__ ll_mask;  // [nb] ranks that read each boundary node
   int lam_ring;  // resident: multiplier regions in shared memory (2, or 8: the last 8 sweeps stay in
                  // shared memory and only the stopping sweep's result is written to gl at exit)
+  int row_skip;  // resident head-first scans: per-row tail budgets (row_budget) in shared memory
 };
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000000000ull;
@@ -799,6 +800,48 @@ __device__ unsigned long long g_head_stats[8];
 #define F2M_HEAD_COUNT(i)
 #endif
 
+template <int MODE>
+__device__ __forceinline__ bool tail_test(double v, double thr, double& tmin) {
+  if (MODE == 1) {
+    tmin = v < tmin ? v : tmin;
+    return false;
+  }
+  return v < thr;
+}
+
+// An upper bound of the warp's largest non-negative double in one REDUX: the max of the high words,
+// rounded up to the next high word (relative overestimate <= 2^-20)
+__device__ __forceinline__ double warp_max_up(double x) {
+  const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(x) >> 32);
+  const unsigned m = __reduce_max_sync(0xffffffffu, x != 0.0 ? hi + 1u : 0u);
+  return __longlong_as_double((long long)((unsigned long long)m << 32));
+}
+
+// Tail skipping (resident head-first scans, interior rows). The tail test of a row only has to prove that every
+// tail slot's reduced cost stays >= the row's threshold s[B]. In exact arithmetic
+// z_j - s[B] = (c_j - l_u) - OS_{B+1}(c_k - l_k) (l_v cancels), so from one sweep to the next it
+// falls by at most 2 D, D = max |l_t - l_{t-1}| over the row's neighbours. A full tail scan at
+// sweep s0 records the margin m = min_tail z - s[B]; while m - 2 (C_s - C_s0) stays above the
+// rounding slack (C = running sum of per-sweep drift bounds of the CTA's own rows: an interior
+// row's neighbours are all own rows, and the CTA's max |d| of each sweep is already reduced for the
+// convergence test), every tail comparison of sweep s is false and only the head is evaluated.
+// Boundary rows keep the plain tail test: bounding their halo's drift put a reduction on the
+// exchange chain (staged -> published -> staged) and cost more than it saved (100k 2.09 -> 2.51 us
+// per sweep, 200k 2.98 -> 2.89; profiles/r02_ncu_sweep.md).
+// Rounding: each computed z and s[B] is within 2.01 u (|c| + |l_v| + |l_u|) of exact, the
+// multipliers stay below L0 + C (L0 = the CTA's largest |l| at the start), so a slack of
+// 1e-12 (cmax + 2 L0 + 2 C) plus a 1e-9 relative allowance on C (its rounded accumulation over
+// <= 1e6 sweeps) is rigorous; the result — which slots the tail compare finds below s[B] (none) —
+// is exactly the one of the full scan, hence bit-identical deltas.
+// The row's budget b = m (1 - 1e-9) + 2 C_s0 (1 - 1e-9) - 1e-12 (S0 + 2 C_s0), S0 = cmax + 2 L0;
+// sweep s skips the tail iff b > 2 C_s (1 + 1e-9). The skip decision is warp-uniform (a warp's
+// rows skip together or scan together: no divergent double path).
+__device__ __forceinline__ double row_budget(double mn, double thr, double cc, double s0) {
+  if (!(mn < CUDART_INF)) return CUDART_INF;  // no tail slots
+  const double m = dsub(mn, thr);
+  return dsub(dadd(dmul(m, 1.0 - 1e-9), dmul(2.0 - 2e-9, cc)), dmul(1e-12, dadd(s0, dmul(2.0, cc))));
+}
+
 // Resident row scan with a "head" of B+2 slots: the row's B+2 smallest slots of an earlier sweep,
 // kept first in the row's shared-memory slot order. A row's smallest reduced costs almost never
 // change membership from one sweep to the next (uniform 10k, per sweep: the top-(B+1) set of 0.09 %
@@ -812,10 +855,13 @@ __device__ unsigned long long g_head_stats[8];
 // The kept multiset — the B+1 smallest reduced costs of the row — does not depend on the visiting
 // order (reduced costs are never -0.0: costs are >= +0 and x - y = -0 only for x = -0), so s[B-1],
 // s[B] and hence delta are bit-identical to the plain insertion over all slots.
-// Returns true when the row must be rescanned.
-template <int B>
+// Returns true when the row must be rescanned. MODE 0: tail slots compared with the threshold;
+// 1: also returns the smallest tail value in *mn (row skipping, below); 2: head only (the tail is
+// proven to stay above the threshold).
+template <int B, int MODE = 0>
 __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, const double* lam,
-                                              const double* cst_s, const ushort4* l4, int lb, int w) {
+                                              const double* cst_s, const ushort4* l4, int lb, int w,
+                                              double* mn = nullptr) {
   constexpr int H = B + 2;
   constexpr int HG = (H + 3) / 4;  // packed-index groups covering the head
   int li[4 * HG];
@@ -848,10 +894,12 @@ __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, co
       for (int i = r & 1; i + 1 < H; i += 2) cas(i, i + 1);
     }
   }
+  if (MODE == 2) return false;
   const double thr = sv[B];
   bool hit = false;
+  double tmin = CUDART_INF;
   int j = H;
-#define F2M_TAILV(jj, idx) (dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[idx]) < thr)
+#define F2M_TAILV(jj, idx) tail_test<MODE>(dsub(dsub(cst_s[lb + 32 * (jj)], lv), lam[idx]), thr, tmin)
   if (H % 4) {  // tail slots of the last head group
 #pragma unroll
     for (int u = 0; u < (4 - H % 4) % 4; ++u)
@@ -872,6 +920,10 @@ __device__ __forceinline__ bool row_scan_head(double (&sv)[B + 2], double lv, co
       if (j + u < w) hit |= F2M_TAILV(j + u, lt[u]);
   }
 #undef F2M_TAILV
+  if (MODE == 1) {
+    *mn = tmin;
+    return tmin < thr;
+  }
   return hit;
 }
 
@@ -909,6 +961,46 @@ __device__ __forceinline__ void row_repair(const double (&sv)[K + 1], double lv,
       ++cnt;
     }
   }
+}
+
+#ifndef F2M_SKIP_WARP
+#define F2M_SKIP_WARP 1
+#endif
+// One resident row through the head-first scan (and, with tail skipping, its budget): the B+1
+// smallest reduced costs into sv.
+template <int B, bool RES, int KB>
+__device__ __forceinline__ void row_head_first(double (&sv)[B + 1], double lv, const double* lam, double* cst_s,
+                                               ushort4* l4, const double* __restrict__ gcost,
+                                               const uint16_t* __restrict__ glid, int lb, int w, bool skip,
+                                               double* budp, double cc, double sk0) {
+  double hv[B + 2];
+  bool rescan;
+  if (skip) {
+    bool ok = *budp > dmul(2.000000002, cc);
+#if F2M_SKIP_WARP  // warp-uniform: the warp's rows skip together or scan together (no divergence)
+    ok = __all_sync(__activemask(), ok);
+#endif
+    if (ok) {
+      F2M_HEAD_COUNT(6);
+      row_scan_head<B, 2>(hv, lv, lam, cst_s, l4, lb, w);
+      rescan = false;
+    } else {
+      F2M_HEAD_COUNT(7);
+      double mn;
+      rescan = row_scan_head<B, 1>(hv, lv, lam, cst_s, l4, lb, w, &mn);
+      *budp = rescan ? -CUDART_INF : row_budget(mn, hv[B], cc, sk0);
+    }
+  } else {
+    rescan = row_scan_head<B>(hv, lv, lam, cst_s, l4, lb, w);
+  }
+  if (rescan) {
+#pragma unroll
+    for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
+    row_scan<B + 1, RES, KB>(hv, lv, lam, cst_s, l4, gcost, glid, lb, w);
+    row_repair<B + 1>(hv, lv, lam, cst_s, l4, lb, w);
+  }
+#pragma unroll
+  for (int i = 0; i <= B; ++i) sv[i] = hv[i];
 }
 
 // Initial slot order of one row (resident form, kernel setup): its B+2 smallest reduced costs at
@@ -1100,6 +1192,7 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   __shared__ volatile int s_exit;
   __shared__ unsigned long long s_word;
   __shared__ uint16_t s_lw[NT / 32][16];  // layout_banks_warp scratch, one per warp
+  __shared__ unsigned long long s_scale[2];  // tail skipping: max |cost|, max |l0| (own + halo)
   // CTAs 0..G-1 own the partition; the last CTA of the launch (alone on its SM) is the master.
   // Multi-GPU: this launch's CTAs are the partition CTAs cta_base.. of g_total.
   const int G = a.npeers ? a.g_total : (int)gridDim.x - 1;
@@ -1117,6 +1210,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // 64-register budget at 1024 threads (A/B figures at the macro definitions)
   constexpr int kBatch = RES ? F2M_RES_BATCH : F2M_STREAM_BATCH;
   constexpr bool kHead = RES && F2M_HEAD_SCAN;  // head-first row scans (row_scan_head)
+  constexpr bool kSkipT = kHead && F2M_BANK_LAYOUT && F2M_ROW_SKIP;
+  // (not in the small-graph PAIR form: 10k 1.75 -> 1.79 us/sweep with it, few interior rows per CTA)
+  const bool kSkip = kSkipT && !PAIR && a.row_skip;
   const int s_lo = a.cta_lo[c], s_hi = a.cta_lo[c + 1], s_int = a.cta_int_hi[c];
   const int p0 = s_lo * 32;
   const int own = max(0, min(s_hi * 32, a.n) - p0);
@@ -1157,10 +1253,13 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   // shared address space (a uintptr_t round trip turned these into generic LD.E loads)
   const size_t slc_off = ((size_t)(reinterpret_cast<unsigned char*>(lid4 + nlid4) - smem) + 15) & ~size_t(15);
   int4* slc = reinterpret_cast<int4*>(smem + slc_off);
+  // tail skipping: one budget per own row after the slice table (host: + 16 + 8 max_local bytes)
+  double* bud = reinterpret_cast<double*>(smem + ((slc_off + 16 * (size_t)(s_hi - s_lo) + 15) & ~size_t(15)));
   const double* __restrict__ gcost = a.scost + slot0;
   const uint16_t* __restrict__ glid = a.slidx + slot0;
   for (int i = tid; i < nh; i += blockDim.x) halo_s[i] = a.halo_pub[h0 + i];
   if (tid == 0) {  // <= ~60 slices per CTA in the resident regime
+    s_scale[0] = s_scale[1] = 0ull;
     int z = 0;
     for (int i = 0; i < s_hi - s_lo; ++i) {
       const int w = a.swidth[s_lo + i];
@@ -1188,6 +1287,18 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       // bank-aware columns
       for (int i = tid; i < nh; i += blockDim.x) regA[own + i] = __ldcg(a.gl + a.halo[h0 + i]);
       __syncthreads();
+      if (kSkip) {  // the rounding-slack scale of the tail budgets
+        double cm = 0.0, lm = 0.0;
+        for (int i = tid; i < nslots; i += blockDim.x)  // padding slots (+inf) give z = +inf exactly
+          if (fabs(cst_s[i]) < CUDART_INF) cm = fmax(cm, fabs(cst_s[i]));
+        for (int i = tid; i < own + nh; i += blockDim.x) lm = fmax(lm, fabs(regA[i]));
+        for (int i = tid; i < own; i += blockDim.x) bud[i] = -CUDART_INF;  // first sweep: full scans
+        const unsigned long long cw = warp_max_nonneg(cm), lw = warp_max_nonneg(lm);
+        if (lane == 0) {
+          atomicMax(&s_scale[0], cw);
+          atomicMax(&s_scale[1], lw);
+        }
+      }
       for (int lp = tid; lp < own; lp += blockDim.x) layout_head(B, cst_s, lid4, slc[lp >> 5], lp & 31, regA[lp], regA);
       __syncthreads();
       // one warp per half-slice (one thread when a slice is wider than 32 slots)
@@ -1289,6 +1400,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   unsigned long long prof[kProfFields] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   int s_stop_final = -1;
+  // tail skipping: running sum of the per-sweep drift bounds (identical in every thread)
+  double c_own = 0.0, sk0 = 0.0;
+  if (kSkip) sk0 = dadd(__longlong_as_double((long long)s_scale[0]), dmul(2.0, __longlong_as_double((long long)s_scale[1])));
   for (int s = 0;; ++s) {
     F2M_PROF_T(t0);
     if (tid == 0) F2M_TRACE_EV(s, 0);
@@ -1301,6 +1415,11 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
       named_sync(2, cthreads);
     }
     double mx = 0.0;
+    if (kSkip && s > 0) {
+      // own rows: |l_s - l_{s-1}| <= eta |d| (1 + 2u) + u |l_s| (the CTA max |d| of sweep s-1)
+      const double dm = warp_max_up(lane < ncw ? red[(s - 1) & 1][lane] : 0.0);
+      c_own = dadd(c_own, dadd(dmul(fabs(a.eta), dm), dmul(1e-15, dadd(sk0, c_own))));
+    }
     if (in_halo_bar) named_sync(3 + (s & 1), halo_bar);  // halo of sweep s staged
     F2M_PROF_T(t1);
     F2M_PROF_ADD(0, t1 - t0);
@@ -1375,15 +1494,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
           // the warp's 32 lanes are the 32 rows of one boundary slice (bstart is slice-aligned):
           // one width, so the interior rows' batches apply without predication
           if (kHead && w > B + 1) {
-            double hv[B + 2];
-            if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), lb, w)) {
-#pragma unroll
-              for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
-              row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
-              row_repair<B + 1>(hv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), lb, w);
-            }
-#pragma unroll
-            for (int i = 0; i <= B; ++i) sv[i] = hv[i];
+            row_head_first<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w, false,
+                                           nullptr, 0.0, 0.0);
           } else {
             row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + (p & 31), gcost, glid, lb, w);
           }
@@ -1426,15 +1538,8 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
 #pragma unroll
       for (int i = 0; i <= B; ++i) sv[i] = CUDART_INF;
       if (kHead && w > B + 1) {
-        double hv[B + 2];
-        if (row_scan_head<B>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w)) {
-#pragma unroll
-          for (int i = 0; i <= B + 1; ++i) hv[i] = CUDART_INF;
-          row_scan<B + 1, RES, kBatch>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
-          row_repair<B + 1>(hv, lv, lam, cst_s, lid4 + sw2.z + lane, lb, w);
-        }
-#pragma unroll
-        for (int i = 0; i <= B; ++i) sv[i] = hv[i];
+        row_head_first<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w, kSkip, bud + lp,
+                                       c_own, sk0);
       } else {
         row_scan<B, RES, kBatch>(sv, lv, lam, cst_s, lid4 + sw2.z + lane, gcost, glid, lb, w);
       }
@@ -1519,8 +1624,9 @@ __global__ void __launch_bounds__(NT, 1) k_gdp_sweep5(Sweep4Args a, Sweep4Ctl* c
   if (tid == 0) s_exit = 1;
 #ifdef F2M_HEAD_STATS
   if (tid == 0 && c == 0)
-    printf("head stats: repaired rows %llu; layout conflicts head %llu / %llu, tail %llu / %llu\n", g_head_stats[1],
-           g_head_stats[2], g_head_stats[4], g_head_stats[3], g_head_stats[5]);
+    printf("head stats: repaired rows %llu; layout conflicts head %llu / %llu, tail %llu / %llu; tail skipped %llu, "
+           "scanned %llu\n", g_head_stats[1], g_head_stats[2], g_head_stats[4], g_head_stats[3], g_head_stats[5],
+           g_head_stats[6], g_head_stats[7]);
 #endif
 }
 
@@ -1770,6 +1876,7 @@ SweepResult run_jacobi(const f2m_graph& g, const f2m_engine_config& cfg, double*
     a.record = d_record;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
     a.lam_ring = t.resident ? t.lam_ring : 2;
+    a.row_skip = t.resident ? t.row_skip : 0;
     a.halo_stride = (t.max_halo + 3) & ~3;
     a.lid4_stride = (int)t.max_cta_lid4;
     a.cta_base = 0;
@@ -2572,6 +2679,7 @@ extern "C" int f2m_sweep_multi_launch(const f2m_graph* g, const f2m_engine_confi
     a.record = nullptr;
     a.lam_stride = (int)((((size_t)t.max_local * sizeof(double) + 15) & ~size_t(15)) / sizeof(double));
     a.lam_ring = t.resident ? t.lam_ring : 2;
+    a.row_skip = t.resident ? t.row_skip : 0;
     a.halo_stride = (t.max_halo + 3) & ~3;
     a.lid4_stride = (int)t.max_cta_lid4;
     a.cta_base = rank * Gp;

@@ -113,6 +113,9 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+#ifndef F2M_ROW_SKIP
+#define F2M_ROW_SKIP 1  // per-row tail budgets of the resident head-first scans (dual.cu row_budget)
+#endif
 #ifndef F2M_LAM_RING8
 #define F2M_LAM_RING8 1
 #endif
@@ -165,6 +168,7 @@ struct Topology {
   int64_t max_cta_lid4 = 0;    // max over CTAs of packed local-index entries (ushort4, widths padded to 4)
   size_t smem_bytes = 0;       // dynamic shared memory of the v2 sweep kernel
   int lam_ring = 2;            // resident: shared-memory multiplier regions (8 when they fit, see dual.cu)
+  int row_skip = 0;            // resident: per-row tail budgets in shared memory (dual.cu row_budget)
   int partition_override = 0;  // > 0: partition CTA count for finalize_topology (multi-GPU replicas)
   ~Topology();
 };
