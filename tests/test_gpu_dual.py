@@ -118,6 +118,41 @@ def test_head_first_scans_vs_oracle_b_and_rule(f2m, orc, b, update):
     assert np.array_equal(np.array(st.lam), lam0)
 
 
+@pytest.mark.parametrize("case", ["uniform_b2", "uniform_b1_paper", "clustered_b3", "rounded_ties"])
+def test_tail_skipping_long_runs_vs_oracle(f2m, orc, case):
+    """Interior-row tail skipping (dual.cu row_budget: a row evaluates only its head while its
+    recorded margin minus twice the CTA's accumulated drift stays above the rounding slack) over
+    long fixed-count runs, where the drift per sweep is small and most rows skip: per-sweep
+    max|delta| and the multipliers after 400 sweeps equal the reference's Jacobi sweeps
+    (dual.cpp:129-167). Rounded integer costs give exact ties (zero margins: those rows never
+    skip); clustered points give uneven drift across CTAs; b = 1 / 3 change the head size."""
+    b, update, eta, sweeps = 2, "midpoint", 0.5, 400
+    if case == "uniform_b1_paper":
+        b, update, eta = 1, "paper-difference", 0.7
+    if case == "clustered_b3":
+        b = 3
+        xy = f2m.generate_clustered_instance(60000, 11).points_array()
+    else:
+        xy = orc.generate_instance(60000, 4242, 1000.0)
+    rounded = case == "rounded_ties"
+    og = orc.build_knn_graph(xy, 10, rounded=rounded)
+    inst = f2m.Instance.from_points(xy)
+    if rounded:
+        inst.mode = f2m.DistanceMode.EUC2D_ROUNDED
+    g = f2m.build_knn_graph(inst, 10)
+    lam0 = orc.initial_state(og, b=b)
+    st = f2m.make_initial_state(g, b=b)
+    assert np.array_equal(np.array(st.lam), lam0)
+    mx, dv = f2m.jacobi_sweeps(g, st, sweeps, b=b, update=update, eta=eta)
+    desc = f2m.last_sweep_kernel_desc()
+    assert "resident" in desc and "two lanes" not in desc, desc
+    for s in range(sweeps):
+        omx, odv = orc.jacobi_sweep(og, lam0, b=b, update=update, eta=eta)
+        assert mx[s] == omx, s
+    assert dv == odv
+    assert np.array_equal(np.array(st.lam), lam0)
+
+
 @pytest.mark.parametrize("k,rounded", [(24, False), (40, True)])
 def test_head_first_scans_wide_rows(f2m, orc, k, rounded):
     """Wide rows (k = 24 / 40: slice widths past 32, many packed-index groups per row, integer
