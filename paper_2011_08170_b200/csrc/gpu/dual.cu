@@ -825,9 +825,9 @@ __device__ __forceinline__ double warp_max_up(double x) {
 // rounding slack (C = running sum of per-sweep drift bounds of the CTA's own rows: an interior
 // row's neighbours are all own rows, and the CTA's max |d| of each sweep is already reduced for the
 // convergence test), every tail comparison of sweep s is false and only the head is evaluated.
-// Boundary rows keep the plain tail test: bounding their halo's drift put a reduction on the
-// exchange chain (staged -> published -> staged) and cost more than it saved (100k 2.09 -> 2.51 us
-// per sweep, 200k 2.98 -> 2.89; profiles/r02_ncu_sweep.md).
+// Boundary rows keep the plain tail test: with them skipping too (their halo's drift reduced by
+// the sync warps or by the boundary warps), the exchange chain (staged -> published -> staged)
+// got longer, 100k 2.09 -> 2.51 us per sweep (200k 2.98 -> 2.89; profiles/r02_ncu_sweep.md).
 // Rounding: each computed z and s[B] is within 2.01 u (|c| + |l_v| + |l_u|) of exact, the
 // multipliers stay below L0 + C (L0 = the CTA's largest |l| at the start), so a slack of
 // 1e-12 (cmax + 2 L0 + 2 C) plus a 1e-9 relative allowance on C (its rounded accumulation over
